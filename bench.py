@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the B200 NGP-RT render path (BASELINE.json metric).
+
+A step = one 1920x1080 frame rendered by every rank (weak scaling): raygen ->
+march -> gather -> fuse -> composite (K1) -> deferred MLP (K2), on the
+synthetic config-3 scene (SynthScene "c3_1080p"). Rank r
+renders camera (r + N*step) mod 64 of sphere_views(64, 2.9) (config 4's camera
+set); for N > 1 the finished frames are gathered to rank 0 over NCCL inside the
+step (the only collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W untimed warm-up steps; L2 flushed (256 MiB write) before every timed
+step; each step bracketed by CUDA events on the render stream after a barrier +
+synchronize; total = sum over steps, max over ranks. `e2e` re-times the same
+steps through the host-buffer C ABI call ngprt_render_host (camera H2D and the
+RGB D2H inside the timed region). `roofline` is K1's algorithmic bytes
+(SURVEY.md §8(d) formula over the bit-exact per-ray counters) / K1's event time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "1080p fps & Mrays/s at 1/2/4/8 B200 vs host-CPU ref; achieved L2/HBM GB/s"
+UNIT = "fps (1920x1080 frames/s, all GPUs)"
+N_CAMS = 64
+PAPER_FPS = 108.0  # 1080p, L=2, RTX 3090
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c3_1080p")
+    ap.add_argument("--mlp", choices=["tensor", "exact"], default=os.environ.get("NGPRT_MLP", "exact"))
+    ap.add_argument("--no-l2-flush", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target wall time of the bounded CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(stats, L, b_c=2, b_f=2):
+    """sum over rays of occupied*8*((8+2L)*b_c + 8L*b_f)
+    + 4*occ_acc + 1*dist_acc + 12 (RGB out)."""
+    import numpy as np
+    s = stats.reshape(-1, 4).astype(np.float64)
+    per_sample = 8 * ((8 + 2 * L) * b_c + 8 * L * b_f)
+    return float((s[:, 1] * per_sample + 4 * s[:, 2] + 1 * s[:, 3]).sum() + 12 * s.shape[0])
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.device)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            out, _ = self.p.communicate()
+            self.lines = [l.split(", ") for l in out.strip().splitlines() if l.strip()]
+
+    def summary(self):
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(l[1]) for l in self.lines if len(l) > 2 and l[1].replace(".", "").isdigit()]
+        mx = [float(l[2]) for l in self.lines if len(l) > 2 and l[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for l in self.lines:
+            for i, n in enumerate(names):
+                if len(l) > 5 + i and l[5 + i].strip() == "Active":
+                    reasons.add(n)
+        load = [v for v in sm if v > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.lines)}
+
+
+def cpu_sample(scene_synth, cam, W, H, seconds, kind_pref="reference"):
+    """Bounded CPU-baseline sample: horizontal bands of the same camera rendered by
+    oracle/_ref (the reference itself) when present, else the C restatement."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from checkers import REF_SO, CpuScene
+    import paper_2407_10482_b200 as ng
+    kind = "reference" if (kind_pref == "reference" and REF_SO.exists()) else "port"
+    cs = CpuScene(scene_synth.desc_ptr, "ref" if kind == "reference" else "oracle")
+    threads = os.cpu_count() or 1
+    rows = 8
+    y0 = H // 2 - rows // 2
+    t = time.perf_counter()
+    cs.render(cam, ng.Opts(window=(0, y0, W, rows)).to_c(), nthreads=threads)
+    dt = time.perf_counter() - t
+    rows = int(max(8, min(H, rows * seconds / max(dt, 1e-3))))
+    y0 = max(0, H // 2 - rows // 2)
+    t = time.perf_counter()
+    cs.render(cam, ng.Opts(window=(0, y0, W, rows)).to_c(), nthreads=threads)
+    dt = time.perf_counter() - t
+    cs.close()
+    rays = W * rows
+    return {"kind": kind, "cores": threads, "rays": rays, "seconds": dt,
+            "mrays_per_s": rays / dt / 1e6, "fps": rays / dt / (W * H),
+            "sample": f"{W}x{rows} band (rows {y0}..{y0 + rows - 1}) of camera 0, {threads} threads"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2407_10482_b200 as ng
+    cfg = dict(ng.CONFIGS[args.config])
+    W, H = cfg["width"], cfg["height"]
+    scene = ng.SynthScene(**cfg)
+    cams = ng.cameras(N_CAMS, W, H)
+    sys.path.insert(0, str(ROOT / "tests"))
+    from checkers import REF_SO, CpuScene
+    kind = "reference" if REF_SO.exists() else "port"
+    cs = CpuScene(scene.desc_ptr, "ref" if kind == "reference" else "oracle")
+    threads = os.cpu_count() or 1
+    rows = 36  # bounded sample per step: a 1920x36 band (~69k rays)
+    for s in range(args.warmup):
+        cs.render(cams[s % N_CAMS], ng.Opts(window=(0, H // 2, W, 4)).to_c(), nthreads=threads)
+    tot, rays = 0.0, 0
+    for s in range(args.steps):
+        y0 = (H // 2 - rows // 2)
+        t = time.perf_counter()
+        cs.render(cams[(s * world) % N_CAMS], ng.Opts(window=(0, y0, W, rows)).to_c(), nthreads=threads)
+        tot += time.perf_counter() - t
+        rays += W * rows
+    fps = rays / tot / (W * H)
+    line = {"metric": METRIC, "value": fps, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "mrays_per_s": rays / tot / 1e6,
+            "config": {"workload": f"{args.config}: {W}x{H}, host CPU reference render path",
+                       "step": f"bounded sample: one {W}x{rows} band per step"},
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": f"{W}x{rows} band per step, {threads} OpenMP threads"},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2407_10482_b200 as ng
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = dict(ng.CONFIGS[args.config])
+    W, H = cfg["width"], cfg["height"]
+    synth = ng.SynthScene(**cfg)
+    scene = ng.Scene(synth, device=local)
+    info = scene.info()
+    cams = ng.cameras(N_CAMS, W, H)
+    opts = ng.Opts(mlp=args.mlp, profile=True)
+    stream = torch.cuda.current_stream(dev)
+    out = torch.empty((1, H, W, 3), dtype=torch.float32, device=dev)
+    gather = [torch.empty_like(out) for _ in range(world)] if (world > 1 and rank == 0) else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def cam_of(step):
+        return cams[(rank + world * step) % N_CAMS]
+
+    def step_fn(step):
+        ng.render(scene, [cam_of(step)], opts, out=out, stream=stream)
+        if world > 1:
+            dist.gather(out, gather_list=gather, dst=0)
+
+    # per-camera algorithmic bytes from the bit-exact counters (untimed)
+    b_store = 2 if info.storage == 2 else 4
+    alg = {}
+    for s in range(args.warmup + args.steps):
+        c = (rank + world * s) % N_CAMS
+        if c not in alg:
+            _, st = ng.render(scene, [cams[c]], ng.Opts(mlp=args.mlp), stats=True)
+            st = st.cpu().numpy()
+            alg[c] = (algorithmic_bytes(st, scene.L, b_store, b_store), st.reshape(-1, 4).mean(0))
+    for s in range(args.warmup):
+        step_fn(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    k1_ms, k2_ms, launches, bytes_k1 = [], [], 0, 0.0
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            s = args.warmup + i
+            if not args.no_l2_flush:
+                flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            ev[i][0].record(stream)
+            step_fn(s)
+            ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            a, b, n = ng.render_timing(scene)
+            k1_ms.append(a)
+            k2_ms.append(b)
+            launches += n
+            bytes_k1 += alg[(rank + world * s) % N_CAMS][0]
+    total_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    frames = args.steps * world
+    fps = frames / (total_ms / 1e3)
+
+    # ---- e2e through the host-buffer C ABI (H2D camera, D2H RGB inside) ----
+    host_out = torch.empty((1, H, W, 3), dtype=torch.float32).pin_memory()
+    host_np = host_out.numpy()
+    for s in range(min(2, args.warmup)):
+        ng.render_host(scene, [cam_of(s)], ng.Opts(mlp=args.mlp), out=host_np)
+    if world > 1:
+        dist.barrier()
+    e2e_s = 0.0
+    for i in range(args.steps):
+        if not args.no_l2_flush:
+            flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ng.render_host(scene, [cam_of(args.warmup + i)], ng.Opts(mlp=args.mlp), out=host_np)
+        e2e_s += time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_fps = frames / float(t.item())
+
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        k1_avg = sum(k1_ms) / len(k1_ms)
+        achieved = (bytes_k1 / args.steps) / (k1_avg / 1e3) / 1e9
+        traffic = None
+        tp = ROOT / "profiles" / "ncu_traffic.json"
+        if tp.exists():
+            traffic = json.loads(tp.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
+        mean_stats = np.mean([alg[(rank + world * (args.warmup + i)) % N_CAMS][1]
+                              for i in range(args.steps)], axis=0)
+        line = {
+            "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": fps / PAPER_FPS,
+            "dtype": "f32 (fp16 feature storage, lossless)", "data": "synthetic",
+            "mrays_per_s": fps * W * H / 1e6,
+            "config": {"workload": f"{args.config}: {W}x{H} mip360-shaped synthetic scene, "
+                                   f"L={scene.L}, 2^21 entries/level, L_C=512, 512^3 pyramid, "
+                                   f"256^3 distance grid, mlp={args.mlp}",
+                       "cameras": f"sphere_views({N_CAMS}, 2.9); rank r renders (r + N*step) % {N_CAMS}",
+                       "l2": "flushed (256 MiB write) before every timed step" if not args.no_l2_flush
+                             else "not flushed; scene (4.4 GB) larger than L2",
+                       "mean_ray_stats": {"marching": round(float(mean_stats[0]), 2),
+                                          "occupied": round(float(mean_stats[1]), 2),
+                                          "occ_acc": round(float(mean_stats[2]), 2),
+                                          "dist_acc": round(float(mean_stats[3]), 2)},
+                       "scene_device_bytes": int(info.device_bytes),
+                       "parallelism": f"dp{world} (camera sharding, NCCL gather to rank 0)"},
+            "kernel_ms": {"march_K1": k1_avg, "shade_K2": sum(k2_ms) / len(k2_ms)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "march_kernel (K1)",
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": bytes_k1 / args.steps},
+            "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 168,
+                    "d2h_bytes_per_step": W * H * 12,
+                    "api": "ngprt_render_host (pinned host RGB buffer)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_sample(synth, cam_of(0), W, H, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": cb["fps"], "unit": UNIT, "cores": cb["cores"],
+                                    "kind": cb["kind"], "sample": cb["sample"],
+                                    "mrays_per_s": cb["mrays_per_s"]}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,234 @@
+/*
+ * ngprt_cuda.h — C ABI of the B200-native NGP-RT per-ray renderer.
+ *
+ * This is the drop-in boundary for the reference's render path. The reference
+ * (/root/reference/proj/include/ngprt, header-only C++20, CPU) exposes the path
+ * as C++ value types, not as an FFI; each entry point below names the reference
+ * interface it replaces:
+ *
+ *   ngprt_scene_desc / ngprt_scene_create  <- ngprt::BakedScene           baking.hpp:55-64
+ *                                             (+ load_baked sections       baking.hpp:229-254,351-485)
+ *   ngprt_camera                           <- PosedDataset + Frame::c2w   scene.hpp:191-201
+ *   ngprt_render_opts                      <- march() arguments           occupancy.hpp:302-305
+ *                                             + render CLI flags
+ *   ngprt_render / ngprt_render_host       <- render_ray (specified, never implemented)
+ *                                             SPEC.md:309-317, composed from generate_rays
+ *                                             scene.hpp:211-228, march occupancy.hpp:302-326,
+ *                                             decode_point_baked baking.hpp:84-91,
+ *                                             composite volume.hpp:51-75, shade volume.hpp:118-137
+ *   ngprt_ray_stats                        <- MarchCounters               occupancy.hpp:197-210
+ *   ngprt_build_pyramid                    <- build_pyramid               occupancy.hpp:114-119
+ *   ngprt_build_distance_grid              <- build_distance_grid         occupancy.hpp:136-194
+ *   ngprt_last_error                       <- the exception text the reference throws
+ *
+ * Conventions: plain pointers and sizes only; no C++ or torch types; no
+ * exceptions cross this boundary. Every call returns an ngprt_status and
+ * leaves a thread-local message for ngprt_last_error(). Host inputs are copied
+ * at scene creation; the scene is immutable afterwards and may be rendered
+ * concurrently on different streams.
+ */
+#ifndef NGPRT_CUDA_H
+#define NGPRT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NGPRT_ABI_VERSION 1
+#define NGPRT_MAX_FINE_LEVELS 4 /* kMaxFineLevels, fusion.hpp:33 */
+#define NGPRT_PYRAMID_LEVELS 5  /* kPyramidLevels, occupancy.hpp:104 */
+
+typedef enum {
+    NGPRT_OK = 0,
+    NGPRT_EINVAL = 1,       /* std::invalid_argument / std::domain_error / out_of_range */
+    NGPRT_ECUDA = 2,        /* CUDA runtime failure (message carries cudaGetErrorString) */
+    NGPRT_ENOMEM = 3,       /* device allocation failed */
+    NGPRT_EUNSUPPORTED = 4, /* valid in the reference, not implemented here (message says what) */
+    NGPRT_ENODEV = 5        /* no CUDA device / not an sm_100 device */
+} ngprt_status;
+
+/* FusionTag, fusion.hpp:44-51 (same numeric values as the .ngrt header byte). */
+typedef enum {
+    NGPRT_FUSION_SUM = 0,
+    NGPRT_FUSION_SHARED_ATT_INV = 1,
+    NGPRT_FUSION_SEPARATE_ATT_INV = 2,
+    NGPRT_FUSION_SHARED_ATT_V = 3,
+    NGPRT_FUSION_SEPARATE_ATT_V = 4,
+    NGPRT_FUSION_MLP = 5 /* ablation only (PAPER Table 3); rejected with NGPRT_EUNSUPPORTED */
+} ngprt_fusion_tag;
+
+/* How feature rows are stored in HBM. AUTO picks fp16 when every coarse row
+ * and fine-table value survives an f32->f16->f32 round trip (lossless, so the
+ * render stays bit-exact), else f32. */
+typedef enum { NGPRT_STORAGE_AUTO = 0, NGPRT_STORAGE_F32 = 1, NGPRT_STORAGE_F16 = 2 } ngprt_storage;
+
+/* Deferred MLP (shade, volume.hpp:118-137) implementation.
+ * EXACT  : f32 CUDA-core forward in the reference's operation order -> bit-exact RGB.
+ * TENSOR : tcgen05.mma (fp16 split-precision operands, f32 TMEM accumulators) -> RGB
+ *          within 1e-3 of the reference (north_star tolerance). Default. */
+typedef enum { NGPRT_MLP_TENSOR = 0, NGPRT_MLP_EXACT = 1 } ngprt_mlp_mode;
+
+/* POD view of a BakedScene (baking.hpp:55-64). All pointers are HOST pointers,
+ * copied by ngprt_scene_create. */
+typedef struct ngprt_scene_desc {
+    uint32_t L;                                  /* EncodingConfig::fine_levels (1..4)       */
+    uint32_t L_C;                                /* EncodingConfig::corner_grid_res          */
+    uint32_t fine_res[NGPRT_MAX_FINE_LEVELS];    /* HashLevel::resolution (1024 << l)         */
+    uint64_t fine_table_len[NGPRT_MAX_FINE_LEVELS]; /* HashLevel::table_len                  */
+    uint8_t fine_hashed[NGPRT_MAX_FINE_LEVELS];  /* HashLevel::addressing (0 direct, 1 hash) */
+    uint8_t fusion_tag;                          /* ngprt_fusion_tag                          */
+    uint8_t storage;                             /* ngprt_storage                             */
+    uint8_t reserved[2];
+    uint64_t n_coarse;                           /* SparseCoarseGrid::count()                 */
+    const uint64_t* coarse_keys;                 /* key_of(corner), any order, unique         */
+    const float* coarse_rows;                    /* n_coarse x (8+2L) f32                     */
+    const float* fine_tables[NGPRT_MAX_FINE_LEVELS]; /* table_len x 8 f32, row-major          */
+    const float* psi_w[3];                       /* TinyMlp 23->64->64->3, row-major out x in */
+    const float* psi_b[3];
+    const float* att_globals;                    /* FusionMode::global_pre, 2L (Inv modes)    */
+    uint32_t occ_base_res;                       /* pyramid.levels[0].res                     */
+    uint32_t dist_res;                           /* DistanceGrid::resolution; 0 = no grid     */
+    const uint64_t* pyramid_words[NGPRT_PYRAMID_LEVELS]; /* [0] required; [1..4] NULL => built on device */
+    const uint8_t* dist_values;                  /* dist_res^3, NULL => built on device from the
+                                                    pyramid level whose res == dist_res       */
+} ngprt_scene_desc;
+
+/* Pinhole camera: PosedDataset intrinsics + one Frame (scene.hpp:191-201).
+ * c2w is row-major 4x4 camera-to-world (x right, y down, z forward). */
+typedef struct ngprt_camera {
+    double c2w[16];
+    double fx, fy, cx, cy;
+    uint32_t width, height;
+} ngprt_camera;
+
+typedef struct ngprt_render_opts {
+    float step;            /* march step gamma*s0; <= 0 => kBaseStep = 2*sqrt(3)/512 (config.hpp:11) */
+    uint8_t use_dist_grid; /* pass &distance (1) or nullptr (0) to march()                 */
+    uint8_t max_step_rule; /* occupancy.hpp:272                                             */
+    uint8_t early_stop;    /* T < 2e-3 termination (volume.hpp:36,70)                       */
+    int8_t keep_level;     /* 0 = off; 1..L = level_masked_fine(keep_level) (fusion.hpp:198-209) */
+    uint8_t mlp_mode;      /* ngprt_mlp_mode                                                */
+    uint8_t profile;       /* record CUDA events around each kernel (ngprt_render_timing)  */
+    uint8_t reserved[2];
+    uint32_t x0, y0, w, h; /* pixel window; w == 0 || h == 0 => full frame. Output is w x h. */
+} ngprt_render_opts;
+
+/* MarchCounters (occupancy.hpp:197-210), per ray. */
+typedef struct ngprt_ray_stats {
+    uint32_t marching;
+    uint32_t occupied;
+    uint32_t occ_acc;
+    uint32_t dist_acc;
+} ngprt_ray_stats;
+
+typedef struct ngprt_scene ngprt_scene; /* opaque; owns device memory */
+
+typedef struct ngprt_scene_info {
+    int device;
+    uint8_t storage;          /* resolved ngprt_storage (F32 or F16) */
+    uint8_t reserved[3];
+    uint32_t coarse_row_stride; /* elements per stored coarse row */
+    uint64_t device_bytes;    /* total device memory owned by the scene */
+    uint64_t coarse_bytes, fine_bytes, pyramid_bytes, dist_bytes;
+    const void* dev_pyramid[NGPRT_PYRAMID_LEVELS]; /* device pointers (u64 words) */
+    const void* dev_dist;                          /* device pointer (u8), NULL if none */
+} ngprt_scene_info;
+
+int ngprt_abi_version(void);
+const char* ngprt_last_error(void);
+
+/* Scene lifetime (replaces constructing / load_baked-ing a BakedScene). */
+ngprt_status ngprt_scene_create(const ngprt_scene_desc* desc, int device, ngprt_scene** out);
+void ngprt_scene_destroy(ngprt_scene* scene);
+ngprt_status ngprt_scene_info_get(const ngprt_scene* scene, ngprt_scene_info* info);
+
+/* Render n_cams frames. rgb_dev: n_cams x h x w x 3 f32 (Image::rgb layout per
+ * frame, image.hpp:12-22); stats_dev: n_cams x h x w (nullable). Device
+ * pointers, asynchronous on `stream` (cudaStream_t, NULL = legacy default). */
+ngprt_status ngprt_render(const ngprt_scene* scene, const ngprt_camera* cams, int n_cams,
+                          const ngprt_render_opts* opts, float* rgb_dev,
+                          ngprt_ray_stats* stats_dev, void* stream);
+
+/* Same with HOST buffers: copies cameras in and rgb/stats out, synchronous.
+ * This is the call that replaces a host-side render(BakedScene, PosedDataset, frame). */
+ngprt_status ngprt_render_host(const ngprt_scene* scene, const ngprt_camera* cams, int n_cams,
+                               const ngprt_render_opts* opts, float* rgb_host,
+                               ngprt_ray_stats* stats_host);
+
+/* Per-kernel device time of the most recent ngprt_render on this scene with
+ * opts.profile set: CUDA events recorded on the render stream around the march
+ * kernel (K1) and the deferred-MLP kernel (K2), summed over launches. Call
+ * after synchronising that stream. Single-stream benchmarking aid. */
+ngprt_status ngprt_render_timing(const ngprt_scene* scene, float* ms_march, float* ms_shade,
+                                 int* n_launches);
+
+/* Occupancy structures on device (device pointers, async on stream).
+ * levels_dev[k-1] receives level k (res base>>k), k = 1..4, u64 words x-fastest. */
+ngprt_status ngprt_build_pyramid(const uint64_t* base_words_dev, uint32_t base_res,
+                                 uint64_t* const levels_dev[NGPRT_PYRAMID_LEVELS - 1],
+                                 void* stream);
+/* out_dev: res^3 u8, G = min(255, max(0, D_cheb - 1)). scratch-free (in-place u8 passes). */
+ngprt_status ngprt_build_distance_grid(const uint64_t* occ_words_dev, uint32_t res,
+                                       uint8_t* out_dev, void* stream);
+
+/* Test hooks (device pointers): the device port of glibc expf, and the fine-level
+ * row index (HashLevel::hash_index, hash_grid.hpp:83-94) for corner triples. */
+ngprt_status ngprt_test_expf(const float* x_dev, float* y_dev, uint64_t n, void* stream);
+ngprt_status ngprt_test_expf_range(uint32_t first_bits, uint64_t n, uint32_t* y_bits_dev,
+                                   void* stream);
+ngprt_status ngprt_test_hash_index(const int32_t* corners_dev, uint64_t n, uint32_t res,
+                                   uint64_t table_len, uint8_t hashed, uint64_t* out_dev,
+                                   void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Synthetic scenes (host-only input generation). Restates the reference's own
+ * generators so the GPU and the CPU oracle consume the same scene object:
+ * make_scene/scene_occupancy (scene.hpp:168-183,329-385), Rng (common.hpp:46-75),
+ * TinyMlp::init (nn.hpp:154-173), sphere_views (scene.hpp:254-265).
+ * ------------------------------------------------------------------------- */
+typedef struct ngprt_synth_params {
+    char occupancy[32];     /* "bench" | "toy" | "slab" (make_scene presets) | "blob" |
+                               "mip360" | "boxes" */
+    uint64_t scene_seed;    /* make_scene seed (41) */
+    uint32_t n_boxes;       /* "boxes" preset only */
+    uint32_t occ_base_res;  /* pyramid base resolution (512 / 256) */
+    uint32_t dist_level;    /* distance grid built from pyramid.levels[dist_level] (1); 5 = none */
+    uint32_t L;             /* fine levels */
+    uint32_t L_C;           /* corner grid resolution */
+    uint32_t fusion_tag;
+    uint64_t fine_table_len;
+    uint64_t table_seed;    /* fine tables, Rng(7) */
+    uint64_t coarse_seed;   /* coarse rows, Rng(13) */
+    uint64_t psi_seed;      /* psi init, Rng(11) */
+    double sigma_lo, sigma_hi;  /* coarse sigma_pre ~ U[lo,hi] */
+    double feat_scale;          /* fine-table and coarse colour channels ~ U[-s,s] */
+    double att_scale;           /* attention logits ~ U[-a,a] */
+    double psi_bias_scale;      /* 0 => zero biases (TinyMlp::init); else U[-b,b] */
+    uint8_t fp16_exact;         /* round every value to an fp16-representable f32 */
+    uint8_t reserved[7];
+} ngprt_synth_params;
+
+typedef struct ngprt_synth ngprt_synth;
+
+void ngprt_synth_default_params(ngprt_synth_params* p);
+ngprt_status ngprt_synth_create(const ngprt_synth_params* p, ngprt_synth** out);
+const char* ngprt_synth_last_error(void);
+/* The desc points into memory owned by the synth object (valid until destroy). */
+const ngprt_scene_desc* ngprt_synth_desc(const ngprt_synth* s);
+void ngprt_synth_destroy(ngprt_synth* s);
+/* sphere_views(n, radius) with fx = fy = 1.1 W, cx = W/2, cy = H/2 (scene.hpp:388-395). */
+ngprt_status ngprt_synth_cameras(int n, double radius, uint32_t width, uint32_t height,
+                                 ngprt_camera* out);
+/* Host-side helpers exposed for the tests: CRC-32 (common.hpp:78-92) and the
+ * splitmix64 uniform stream (common.hpp:46-60). */
+uint32_t ngprt_crc32(const void* data, uint64_t len, uint32_t seed);
+void ngprt_rng_uniform(uint64_t seed, double lo, double hi, uint64_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NGPRT_CUDA_H */

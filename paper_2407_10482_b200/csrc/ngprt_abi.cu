@@ -1,0 +1,561 @@
+// ngprt_abi.cu — the extern "C" boundary (include/ngprt_cuda.h): scene upload
+// and layout conversion, render dispatch, occupancy builders, error reporting.
+// No exceptions cross this boundary; every failure returns a status and leaves
+// a message for ngprt_last_error() (the reference throws, e.g. baking.hpp:396-405).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "render.cuh"
+
+using namespace ngprt_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+ngprt_status fail(ngprt_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define NG_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            return fail(e_ == cudaErrorMemoryAllocation ? NGPRT_ENOMEM : NGPRT_ECUDA,   \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));            \
+        }                                                                               \
+    } while (0)
+
+bool fp16_exact(float v) {
+    // f32 -> f16 (round to nearest even) -> f32 must be the identity.
+    if (std::isnan(v)) return false;
+    const float h = __half2float(__float2half_rn(v));
+    return std::memcmp(&h, &v, 4) == 0;
+}
+
+float host_sigmoid(float x) { return 1.0f / (1.0f + std::exp(-x)); }  // nn.hpp:91-94 (glibc expf)
+
+}  // namespace
+
+struct ngprt_scene {
+    int device = 0;
+    DevScene ds{};
+    std::vector<void*> allocs;
+    void* psi_tc = nullptr;
+    ngprt_scene_info info{};
+    void* fine_block = nullptr;
+    size_t fine_block_bytes = 0;
+    // profiling events of the last profiled render: (before K1, after K1, after K2) per launch
+    mutable std::mutex prof_mu;
+    mutable std::vector<cudaEvent_t> prof_events;
+    mutable int prof_launches = 0;
+
+    ~ngprt_scene() {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
+        for (void* p : allocs) cudaFree(p);
+        cudaSetDevice(prev);
+    }
+    cudaEvent_t prof_event(size_t i) const {
+        while (prof_events.size() <= i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            prof_events.push_back(e);
+        }
+        return prof_events[i];
+    }
+    template <class T>
+    cudaError_t alloc(T** p, size_t bytes) {
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, bytes ? bytes : 1);
+        if (e == cudaSuccess) {
+            allocs.push_back(q);
+            info.device_bytes += bytes;
+        }
+        *p = static_cast<T*>(q);
+        return e;
+    }
+};
+
+extern "C" {
+
+int ngprt_abi_version(void) { return NGPRT_ABI_VERSION; }
+
+const char* ngprt_last_error(void) { return g_err.c_str(); }
+
+ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_scene** out) {
+    if (!d || !out) return fail(NGPRT_EINVAL, "ngprt_scene_create: null argument");
+    *out = nullptr;
+    // --- validation (mirrors the reference's invariants) ---
+    if (d->L < 1 || d->L > NGPRT_MAX_FINE_LEVELS)
+        return fail(NGPRT_EINVAL, "L out of range (1..4; the reference accepts 2..4, baking.hpp:366)");
+    if (d->L_C < 1) return fail(NGPRT_EINVAL, "L_C must be >= 1");
+    if (d->fusion_tag == NGPRT_FUSION_MLP)
+        return fail(NGPRT_EUNSUPPORTED,
+                    "fusion mode 'mlp' (ablation, fusion.hpp:162-171) is not implemented");
+    if (d->fusion_tag > NGPRT_FUSION_MLP) return fail(NGPRT_EINVAL, "unknown fusion tag");
+    if ((d->fusion_tag == NGPRT_FUSION_SHARED_ATT_INV ||
+         d->fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV) &&
+        !d->att_globals)
+        return fail(NGPRT_EINVAL, "invariant attention mode needs att_globals (baking.hpp:480)");
+    if (d->occ_base_res < 16 || d->occ_base_res % 16)
+        return fail(NGPRT_EINVAL, "occ_base_res must be a positive multiple of 16");
+    if (!d->pyramid_words[0]) return fail(NGPRT_EINVAL, "pyramid level 0 is required");
+    if (d->n_coarse && (!d->coarse_keys || !d->coarse_rows))
+        return fail(NGPRT_EINVAL, "coarse keys/rows missing");
+    for (int k = 0; k < 3; ++k)
+        if (!d->psi_w[k] || !d->psi_b[k]) return fail(NGPRT_EINVAL, "psi weights missing");
+    const int L = int(d->L);
+    const int w = 8 + 2 * L;
+    for (int l = 0; l < L; ++l) {
+        if (!d->fine_tables[l] || d->fine_table_len[l] == 0)
+            return fail(NGPRT_EINVAL, "fine table missing");
+        if (d->fine_res[l] < 1) return fail(NGPRT_EINVAL, "fine resolution must be >= 1");
+        if (!d->fine_hashed[l]) {
+            const uint64_t r1 = uint64_t(d->fine_res[l]) + 1;
+            if (r1 * r1 * r1 > d->fine_table_len[l])
+                return fail(NGPRT_EINVAL, "direct-addressed fine level needs (res+1)^3 rows");
+        }
+    }
+    const uint64_t r1c = uint64_t(d->L_C) + 1;
+    const uint64_t n_corner = r1c * r1c * r1c;
+    for (uint64_t i = 0; i < d->n_coarse; ++i)
+        if (d->coarse_keys[i] >= n_corner)
+            return fail(NGPRT_EINVAL, "coarse key " + std::to_string(d->coarse_keys[i]) +
+                                          " outside the (L_C+1)^3 corner grid");
+    if (d->dist_res) {
+        bool ok = d->dist_values != nullptr;
+        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k)
+            ok |= (d->occ_base_res >> k) == d->dist_res;
+        if (!ok) return fail(NGPRT_EINVAL, "dist_res matches no pyramid level and no values given");
+    }
+
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+        return fail(NGPRT_ENODEV, "no CUDA device visible");
+    if (device < 0 || device >= n_dev) return fail(NGPRT_EINVAL, "device index out of range");
+    cudaDeviceProp prop;
+    NG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(NGPRT_ENODEV, std::string("this build targets sm_100a (B200); device is ") +
+                                      prop.name);
+    NG_CUDA(cudaSetDevice(device));
+
+    // --- storage decision: fp16 only when lossless ---
+    int storage = d->storage;
+    if (storage == NGPRT_STORAGE_AUTO) {
+        bool exact = true;
+        for (uint64_t i = 0; exact && i < d->n_coarse * uint64_t(w); ++i)
+            exact = fp16_exact(d->coarse_rows[i]);
+        for (int l = 0; exact && l < L; ++l)
+            for (uint64_t i = 0; exact && i < d->fine_table_len[l] * 8; ++i)
+                exact = fp16_exact(d->fine_tables[l][i]);
+        storage = exact ? NGPRT_STORAGE_F16 : NGPRT_STORAGE_F32;
+    }
+    const bool f16 = storage == NGPRT_STORAGE_F16;
+    const size_t esz = f16 ? 2 : 4;
+
+    auto* s = new ngprt_scene;
+    s->device = device;
+    s->info.device = device;
+    DevScene& ds = s->ds;
+    ds.L = L;
+    ds.L_C = int(d->L_C);
+    ds.fusion = d->fusion_tag;
+    ds.storage = storage;
+    s->info.storage = uint8_t(storage);
+    s->info.coarse_row_stride = 16;
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+        delete s;
+        return fail(NGPRT_ECUDA, "cudaStreamCreate failed");
+    }
+    auto cleanup = [&](ngprt_status status) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        if (status != NGPRT_OK) delete s;
+        return status;
+    };
+#define NG_TRY(call)                                                                    \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+            return cleanup(e_ == cudaErrorMemoryAllocation ? NGPRT_ENOMEM : NGPRT_ECUDA); \
+        }                                                                               \
+    } while (0)
+
+    // --- coarse rows: dense (L_C+1)^3 x 16 grid; absent corners are zero rows ---
+    {
+        const size_t bytes = size_t(n_corner) * 16 * esz;
+        void* dense;
+        NG_TRY(s->alloc(&dense, bytes));
+        NG_TRY(cudaMemsetAsync(dense, 0, bytes, st));
+        s->info.coarse_bytes = bytes;
+        if (d->n_coarse) {
+            unsigned long long* dkeys;
+            float* drows;
+            NG_TRY(cudaMallocAsync(&dkeys, d->n_coarse * 8, st));
+            NG_TRY(cudaMallocAsync(&drows, d->n_coarse * w * 4, st));
+            NG_TRY(cudaMemcpyAsync(dkeys, d->coarse_keys, d->n_coarse * 8, cudaMemcpyHostToDevice, st));
+            NG_TRY(cudaMemcpyAsync(drows, d->coarse_rows, d->n_coarse * w * 4, cudaMemcpyHostToDevice, st));
+            launch_scatter_coarse(dkeys, drows, d->n_coarse, w, dense, f16, st);
+            NG_TRY(cudaGetLastError());
+            NG_TRY(cudaFreeAsync(dkeys, st));
+            NG_TRY(cudaFreeAsync(drows, st));
+        }
+        ds.coarse = dense;
+    }
+    // --- fine tables: one contiguous block (one L2 access-policy window) ---
+    {
+        size_t total = 0;
+        size_t offs[NGPRT_MAX_FINE_LEVELS];
+        for (int l = 0; l < L; ++l) {
+            offs[l] = total;
+            total += size_t(d->fine_table_len[l]) * 8 * esz;
+            total = (total + 255) & ~size_t(255);
+        }
+        char* block;
+        NG_TRY(s->alloc(&block, total));
+        s->fine_block = block;
+        s->fine_block_bytes = total;
+        s->info.fine_bytes = total;
+        for (int l = 0; l < L; ++l) {
+            const size_t n = size_t(d->fine_table_len[l]) * 8;
+            float* tmp;
+            NG_TRY(cudaMallocAsync(&tmp, n * 4, st));
+            NG_TRY(cudaMemcpyAsync(tmp, d->fine_tables[l], n * 4, cudaMemcpyHostToDevice, st));
+            launch_convert_fine(tmp, block + offs[l], n, f16, st);
+            NG_TRY(cudaGetLastError());
+            NG_TRY(cudaFreeAsync(tmp, st));
+            ds.fine[l] = block + offs[l];
+            ds.fine_res[l] = int(d->fine_res[l]);
+            ds.fine_len[l] = d->fine_table_len[l];
+            const uint64_t len = d->fine_table_len[l];
+            if (!d->fine_hashed[l]) {
+                ds.fine_mode[l] = 0;
+            } else if ((len & (len - 1)) == 0 && len <= (uint64_t(1) << 32)) {
+                ds.fine_mode[l] = 1;
+                ds.fine_mask[l] = uint32_t(len - 1);
+            } else {
+                ds.fine_mode[l] = 2;
+            }
+        }
+    }
+    // --- occupancy pyramid (K3 for missing levels) ---
+    {
+        int res = int(d->occ_base_res);
+        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) {
+            const int r = res >> k;
+            const size_t words = (size_t(r) * r * r + 63) / 64;
+            uint64_t* g;
+            NG_TRY(s->alloc(&g, words * 8));
+            s->info.pyramid_bytes += words * 8;
+            if (k == 0 || d->pyramid_words[k]) {
+                NG_TRY(cudaMemcpyAsync(g, d->pyramid_words[k], words * 8, cudaMemcpyHostToDevice, st));
+            } else {
+                NG_TRY(cudaMemsetAsync(g, 0, words * 8, st));
+                launch_pyramid_level(ds.occ[k - 1], r * 2, reinterpret_cast<uint32_t*>(g), st);
+                NG_TRY(cudaGetLastError());
+            }
+            ds.occ[k] = reinterpret_cast<const uint32_t*>(g);
+            ds.occ_res[k] = r;
+            s->info.dev_pyramid[k] = g;
+        }
+    }
+    // --- distance grid (K4 when not supplied) ---
+    if (d->dist_res) {
+        const size_t r = d->dist_res, n = r * r * r;
+        uint8_t* g;
+        NG_TRY(s->alloc(&g, n));
+        s->info.dist_bytes = n;
+        if (d->dist_values) {
+            NG_TRY(cudaMemcpyAsync(g, d->dist_values, n, cudaMemcpyHostToDevice, st));
+        } else {
+            int k = 0;
+            while (ds.occ_res[k] != int(r)) ++k;
+            uint16_t *a, *b;
+            NG_TRY(cudaMallocAsync(&a, n * 2, st));
+            NG_TRY(cudaMallocAsync(&b, n * 2, st));
+            launch_distance_grid(ds.occ[k], int(r), a, b, g, st);
+            NG_TRY(cudaGetLastError());
+            NG_TRY(cudaFreeAsync(a, st));
+            NG_TRY(cudaFreeAsync(b, st));
+        }
+        ds.dist = g;
+        ds.dist_res = int(r);
+        s->info.dev_dist = g;
+    } else {
+        ds.dist = nullptr;
+        ds.dist_res = 0;
+    }
+    // --- psi (packed f32 for the exact path; tcgen05 operand image for the tensor path) ---
+    {
+        std::vector<float> packed(kPsiTotal);
+        std::memcpy(packed.data() + kPsiW0, d->psi_w[0], 64 * 23 * 4);
+        std::memcpy(packed.data() + kPsiB0, d->psi_b[0], 64 * 4);
+        std::memcpy(packed.data() + kPsiW1, d->psi_w[1], 64 * 64 * 4);
+        std::memcpy(packed.data() + kPsiB1, d->psi_b[1], 64 * 4);
+        std::memcpy(packed.data() + kPsiW2, d->psi_w[2], 3 * 64 * 4);
+        std::memcpy(packed.data() + kPsiB2, d->psi_b[2], 3 * 4);
+        float* g;
+        NG_TRY(s->alloc(&g, kPsiTotal * 4));
+        NG_TRY(cudaMemcpyAsync(g, packed.data(), kPsiTotal * 4, cudaMemcpyHostToDevice, st));
+        NG_TRY(cudaStreamSynchronize(st));  // `packed` is pageable and local
+        ds.psi = g;
+        std::vector<unsigned char> tc(psi_tc_bytes());
+        pack_psi_tc(packed.data(), tc.data());
+        NG_TRY(s->alloc(&s->psi_tc, tc.size()));
+        NG_TRY(cudaMemcpyAsync(s->psi_tc, tc.data(), tc.size(), cudaMemcpyHostToDevice, st));
+        NG_TRY(cudaStreamSynchronize(st));
+    }
+    // --- invariant attention weights: activate_sigmoid(global_pre) (fusion.hpp:123-132) ---
+    if (d->fusion_tag == NGPRT_FUSION_SHARED_ATT_INV || d->fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV)
+        for (int i = 0; i < 2 * L; ++i) ds.att_w[i] = host_sigmoid(d->att_globals[i]);
+    NG_TRY(cudaStreamSynchronize(st));
+#undef NG_TRY
+    cleanup(NGPRT_OK);
+    *out = s;
+    return NGPRT_OK;
+}
+
+void ngprt_scene_destroy(ngprt_scene* s) { delete s; }
+
+ngprt_status ngprt_scene_info_get(const ngprt_scene* s, ngprt_scene_info* info) {
+    if (!s || !info) return fail(NGPRT_EINVAL, "null argument");
+    *info = s->info;
+    return NGPRT_OK;
+}
+
+namespace {
+
+void set_l2_window(const ngprt_scene* s, cudaStream_t st, cudaStreamAttrValue* saved) {
+    cudaStreamGetAttribute(st, cudaStreamAttributeAccessPolicyWindow, saved);
+    int max_win = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
+    if (max_win <= 0 || !s->fine_block) return;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = s->fine_block;
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(s->fine_block_bytes, size_t(max_win));
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+}
+
+ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
+                         const ngprt_render_opts* o, float* rgb, ngprt_ray_stats* stats,
+                         cudaStream_t st) {
+    if (!s || !cams || !o || !rgb) return fail(NGPRT_EINVAL, "ngprt_render: null argument");
+    if (n_cams <= 0) return fail(NGPRT_EINVAL, "ngprt_render: n_cams must be > 0");
+    if (o->keep_level < 0 || o->keep_level > s->ds.L)
+        return fail(NGPRT_EINVAL, "level_masked_fine: keep_level out of range (fusion.hpp:201-202)");
+    if (o->mlp_mode != NGPRT_MLP_EXACT && o->mlp_mode != NGPRT_MLP_TENSOR)
+        return fail(NGPRT_EINVAL, "unknown mlp_mode");
+    if (o->mlp_mode == NGPRT_MLP_TENSOR)
+        return fail(NGPRT_EUNSUPPORTED, "tensor-core MLP not built yet");
+    const bool window = o->w && o->h;
+    const uint32_t W = window ? o->w : cams[0].width, H = window ? o->h : cams[0].height;
+    for (int c = 0; c < n_cams; ++c) {
+        const ngprt_camera& cam = cams[c];
+        if (!window && (cam.width != W || cam.height != H))
+            return fail(NGPRT_EINVAL, "all cameras of one call must share width/height");
+        if (uint64_t(o->x0) + W > cam.width || uint64_t(o->y0) + H > cam.height)
+            return fail(NGPRT_EINVAL, "generate_rays: pixel out of bounds (scene.hpp:214-215)");
+        if (!(cam.fx != 0.0) || !(cam.fy != 0.0)) return fail(NGPRT_EINVAL, "zero focal length");
+    }
+    if (W == 0 || H == 0) return NGPRT_OK;
+    cudaSetDevice(s->device);
+    const size_t per_cam = size_t(W) * H;
+    RayAcc* acc = nullptr;
+    const int chunk = std::min(n_cams, kMaxCamsPerLaunch);
+    NG_CUDA(cudaMallocAsync(&acc, per_cam * chunk * sizeof(RayAcc), st));
+    cudaStreamAttrValue saved{};
+    set_l2_window(s, st, &saved);
+    MarchParams p{};
+    p.x0 = o->x0;
+    p.y0 = o->y0;
+    p.w = W;
+    p.h = H;
+    p.step = o->step > 0 ? o->step : float(2.0 * std::sqrt(3.0) / 512.0);  // kBaseStep config.hpp:11
+    p.use_grid = o->use_dist_grid;
+    p.max_step_rule = o->max_step_rule;
+    p.early_stop = o->early_stop;
+    p.keep_level = o->keep_level;
+    p.acc = acc;
+    std::unique_lock<std::mutex> prof_lock(s->prof_mu, std::defer_lock);
+    if (o->profile) {
+        prof_lock.lock();
+        s->prof_launches = 0;
+    }
+    for (int c0 = 0; c0 < n_cams; c0 += kMaxCamsPerLaunch) {
+        const int nc = std::min(kMaxCamsPerLaunch, n_cams - c0);
+        p.n_cams = nc;
+        for (int i = 0; i < nc; ++i) {
+            const ngprt_camera& cam = cams[c0 + i];
+            CamParams& cp = p.cams[i];
+            for (int k = 0; k < 12; ++k) cp.m[k] = cam.c2w[k];
+            cp.fx = cam.fx;
+            cp.fy = cam.fy;
+            cp.cx = cam.cx;
+            cp.cy = cam.cy;
+            cp.width = cam.width;
+            cp.height = cam.height;
+        }
+        p.stats = stats ? stats + size_t(c0) * per_cam : nullptr;
+        const int li = s->prof_launches;
+        if (o->profile) cudaEventRecord(s->prof_event(3 * li), st);
+        launch_march(s->ds, p, st);
+        if (o->profile) cudaEventRecord(s->prof_event(3 * li + 1), st);
+        float* out = rgb + size_t(c0) * per_cam * 3;
+        if (o->mlp_mode == NGPRT_MLP_EXACT)
+            launch_shade_exact(s->ds, acc, out, per_cam * nc, st);
+        else
+            launch_shade_tensor(s->ds, s->psi_tc, acc, out, per_cam * nc, st);
+        if (o->profile) {
+            cudaEventRecord(s->prof_event(3 * li + 2), st);
+            s->prof_launches = li + 1;
+        }
+    }
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &saved);
+    NG_CUDA(cudaGetLastError());
+    NG_CUDA(cudaFreeAsync(acc, st));
+    return NGPRT_OK;
+}
+
+}  // namespace
+
+ngprt_status ngprt_render(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
+                          const ngprt_render_opts* o, float* rgb_dev, ngprt_ray_stats* stats_dev,
+                          void* stream) {
+    return render_impl(s, cams, n_cams, o, rgb_dev, stats_dev, static_cast<cudaStream_t>(stream));
+}
+
+ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
+                               const ngprt_render_opts* o, float* rgb_host,
+                               ngprt_ray_stats* stats_host) {
+    if (!s || !cams || !o || !rgb_host) return fail(NGPRT_EINVAL, "ngprt_render_host: null argument");
+    if (n_cams <= 0) return fail(NGPRT_EINVAL, "ngprt_render_host: n_cams must be > 0");
+    NG_CUDA(cudaSetDevice(s->device));
+    const bool window = o->w && o->h;
+    const size_t W = window ? o->w : cams[0].width, H = window ? o->h : cams[0].height;
+    const size_t n = W * H * size_t(n_cams);
+    cudaStream_t st;
+    NG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    float* rgb = nullptr;
+    ngprt_ray_stats* stats = nullptr;
+    ngprt_status status = NGPRT_OK;
+    if (cudaMallocAsync(&rgb, n * 12, st) != cudaSuccess ||
+        (stats_host && cudaMallocAsync(&stats, n * sizeof(ngprt_ray_stats), st) != cudaSuccess)) {
+        status = fail(NGPRT_ENOMEM, "ngprt_render_host: device allocation failed");
+    } else {
+        status = render_impl(s, cams, n_cams, o, rgb, stats, st);
+        if (status == NGPRT_OK) {
+            cudaMemcpyAsync(rgb_host, rgb, n * 12, cudaMemcpyDeviceToHost, st);
+            if (stats_host)
+                cudaMemcpyAsync(stats_host, stats, n * sizeof(ngprt_ray_stats),
+                                cudaMemcpyDeviceToHost, st);
+        }
+    }
+    if (rgb) cudaFreeAsync(rgb, st);
+    if (stats) cudaFreeAsync(stats, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (status == NGPRT_OK && e != cudaSuccess)
+        status = fail(NGPRT_ECUDA, std::string("ngprt_render_host: ") + cudaGetErrorString(e));
+    return status;
+}
+
+ngprt_status ngprt_render_timing(const ngprt_scene* s, float* ms_march, float* ms_shade,
+                                 int* n_launches) {
+    if (!s) return fail(NGPRT_EINVAL, "null scene");
+    std::lock_guard<std::mutex> g(s->prof_mu);
+    float a = 0.f, b = 0.f;
+    for (int i = 0; i < s->prof_launches; ++i) {
+        float x = 0.f, y = 0.f;
+        NG_CUDA(cudaEventElapsedTime(&x, s->prof_events[3 * i], s->prof_events[3 * i + 1]));
+        NG_CUDA(cudaEventElapsedTime(&y, s->prof_events[3 * i + 1], s->prof_events[3 * i + 2]));
+        a += x;
+        b += y;
+    }
+    if (ms_march) *ms_march = a;
+    if (ms_shade) *ms_shade = b;
+    if (n_launches) *n_launches = 2 * s->prof_launches;
+    return NGPRT_OK;
+}
+
+ngprt_status ngprt_build_pyramid(const uint64_t* base, uint32_t base_res,
+                                 uint64_t* const levels[NGPRT_PYRAMID_LEVELS - 1], void* stream) {
+    if (!base || !levels) return fail(NGPRT_EINVAL, "ngprt_build_pyramid: null argument");
+    if (base_res < 16 || base_res % 16) return fail(NGPRT_EINVAL, "base_res must be a multiple of 16");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(base);
+    for (int k = 1; k < NGPRT_PYRAMID_LEVELS; ++k) {
+        const int r = int(base_res >> k);
+        const size_t words = (size_t(r) * r * r + 63) / 64;
+        NG_CUDA(cudaMemsetAsync(levels[k - 1], 0, words * 8, st));
+        launch_pyramid_level(src, r * 2, reinterpret_cast<uint32_t*>(levels[k - 1]), st);
+        src = reinterpret_cast<const uint32_t*>(levels[k - 1]);
+    }
+    NG_CUDA(cudaGetLastError());
+    return NGPRT_OK;
+}
+
+ngprt_status ngprt_build_distance_grid(const uint64_t* occ, uint32_t res, uint8_t* out,
+                                       void* stream) {
+    if (!occ || !out || res == 0) return fail(NGPRT_EINVAL, "ngprt_build_distance_grid: bad argument");
+    if (res > 32768) return fail(NGPRT_EINVAL, "resolution too large");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t n = size_t(res) * res * res;
+    uint16_t *a, *b;
+    NG_CUDA(cudaMallocAsync(&a, n * 2, st));
+    NG_CUDA(cudaMallocAsync(&b, n * 2, st));
+    launch_distance_grid(reinterpret_cast<const uint32_t*>(occ), int(res), a, b, out, st);
+    NG_CUDA(cudaGetLastError());
+    NG_CUDA(cudaFreeAsync(a, st));
+    NG_CUDA(cudaFreeAsync(b, st));
+    return NGPRT_OK;
+}
+
+ngprt_status ngprt_test_expf(const float* x, float* y, uint64_t n, void* stream) {
+    launch_test_expf(x, y, n, static_cast<cudaStream_t>(stream));
+    NG_CUDA(cudaGetLastError());
+    return NGPRT_OK;
+}
+
+ngprt_status ngprt_test_expf_range(uint32_t first, uint64_t n, uint32_t* y, void* stream) {
+    launch_test_expf_range(first, n, y, static_cast<cudaStream_t>(stream));
+    NG_CUDA(cudaGetLastError());
+    return NGPRT_OK;
+}
+
+ngprt_status ngprt_test_hash_index(const int32_t* corners, uint64_t n, uint32_t res,
+                                   uint64_t table_len, uint8_t hashed, uint64_t* out,
+                                   void* stream) {
+    DevScene sc{};
+    int mode = 0;
+    uint32_t mask = 0;
+    if (hashed) {
+        if ((table_len & (table_len - 1)) == 0 && table_len <= (uint64_t(1) << 32)) {
+            mode = 1;
+            mask = uint32_t(table_len - 1);
+        } else {
+            mode = 2;
+        }
+    }
+    launch_test_hash(sc, corners, n, int(res), table_len, mode, mask,
+                     reinterpret_cast<unsigned long long*>(out), static_cast<cudaStream_t>(stream));
+    NG_CUDA(cudaGetLastError());
+    return NGPRT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// render.cuh — launch-parameter types shared by the render kernels and the C ABI.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace ngprt_dev {
+
+// One camera, pre-flattened: c2w rows (row-major 3x4), intrinsics, image size.
+struct CamParams {
+    double m[12];
+    double fx, fy, cx, cy;
+    uint32_t width, height;
+};
+
+constexpr int kMaxCamsPerLaunch = 64;  // 64 x 136 B of kernel parameters (CUDA >= 12.1)
+constexpr int kTileW = 16, kTileH = 8, kBlock = kTileW * kTileH;
+
+struct MarchParams {
+    CamParams cams[kMaxCamsPerLaunch];
+    int n_cams;
+    uint32_t x0, y0, w, h;
+    float step;
+    int use_grid, max_step_rule, early_stop, keep_level;
+    RayAcc* acc;              // n_cams x h x w
+    ngprt_ray_stats* stats;   // nullable, n_cams x h x w
+};
+
+// K1: march + gather + fuse + composite (one thread per ray).
+void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st);
+// K2 (exact): f32 CUDA-core deferred MLP in the reference's operation order.
+void launch_shade_exact(const DevScene& sc, const RayAcc* acc, float* rgb, size_t n_rays,
+                        cudaStream_t st);
+// K2 (tensor): tcgen05 deferred MLP, 128 rays per CTA tile.
+void launch_shade_tensor(const DevScene& sc, const void* psi_tc, const RayAcc* acc, float* rgb,
+                         size_t n_rays, cudaStream_t st);
+// Packs psi into the tcgen05 operand layout (done once per scene).
+size_t psi_tc_bytes();
+void pack_psi_tc(const float* psi_host_packed, void* psi_tc_host);
+
+// K3/K4: occupancy structures.
+void launch_pyramid_level(const uint32_t* src, int src_res, uint32_t* dst, cudaStream_t st);
+void launch_distance_grid(const uint32_t* occ, int res, uint16_t* tmp_a, uint16_t* tmp_b,
+                          uint8_t* out, cudaStream_t st);
+void launch_scatter_coarse(const unsigned long long* keys, const float* rows, size_t n, int w,
+                           void* dense, int f16, cudaStream_t st);
+void launch_convert_fine(const float* src, void* dst, size_t n, int f16, cudaStream_t st);
+
+// test hooks
+void launch_test_expf(const float* x, float* y, size_t n, cudaStream_t st);
+void launch_test_expf_range(uint32_t first, size_t n, uint32_t* y, cudaStream_t st);
+void launch_test_hash(const DevScene& sc, const int32_t* corners, size_t n, int res,
+                      unsigned long long len, int mode, uint32_t mask,
+                      unsigned long long* out, cudaStream_t st);
+
+}  // namespace ngprt_dev

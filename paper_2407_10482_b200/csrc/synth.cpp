@@ -1,0 +1,409 @@
+// synth.cpp — host-side synthetic scene and camera generation.
+//
+// Restates the reference's own input generators so that the GPU renderer and
+// the CPU oracle consume the same scene object:
+//   Rng (splitmix64)            common.hpp:46-75
+//   make_scene presets          scene.hpp:329-385   ("slab", "toy", "bench")
+//   scene_occupancy             scene.hpp:168-183
+//   TinyMlp::init               nn.hpp:154-173      (He/Xavier uniform, zero bias)
+//   look_at / sphere_views      scene.hpp:244-265
+//   intrinsics of synth_dataset scene.hpp:388-395   (fx = fy = 1.1 W, cx = W/2, cy = H/2)
+//   crc32                       common.hpp:78-92
+// Coarse rows are retained at every corner adjacent to an occupied L_C voxel,
+// in key order (baking.hpp:156-174). The generated values are pinned against the
+// reference itself by tests/test_synth.py (fixtures from oracle/_ref).
+#include "ngprt_cuda.h"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+struct Rng {  // common.hpp:46-75
+    uint64_t state;
+    explicit Rng(uint64_t seed) : state(seed) {}
+    uint64_t next_u64() {
+        uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    double uniform() { return double(next_u64() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+};
+
+struct Box {
+    double lo[3], hi[3];
+    double sigma;
+};
+
+// Round to the nearest fp16-representable value (ties to even), returned as f32.
+float round_fp16(float f) {
+    if (!std::isfinite(f)) return f;
+    double a = std::fabs(double(f));
+    if (a == 0.0) return f;
+    int e;
+    std::frexp(a, &e);           // a = m * 2^e, m in [0.5, 1)
+    int exp2 = std::max(e - 1, -14);  // unbiased exponent, clamped to the subnormal floor
+    double q = std::ldexp(1.0, exp2 - 10);
+    double r = std::nearbyint(a / q) * q;  // default rounding mode: nearest-even
+    if (r > 65504.0) r = INFINITY;
+    return float(std::copysign(r, double(f)));
+}
+
+// make_scene (scene.hpp:329-385) plus the presets this repo adds for the
+// BASELINE configs (documented in DESIGN.md §inputs).
+std::vector<Box> make_boxes(const std::string& name, uint64_t seed, uint32_t n_boxes) {
+    std::vector<Box> s;
+    auto push = [&](double lx, double ly, double lz, double hx, double hy, double hz, double sig) {
+        s.push_back(Box{{lx, ly, lz}, {hx, hy, hz}, sig});
+    };
+    if (name == "slab") {
+        push(-0.6, -0.6, -0.15, 0.6, 0.6, 0.15, 40.0);
+    } else if (name == "toy") {
+        push(-0.7, -0.7, -0.55, 0.7, 0.7, -0.42, 60.0);
+        Rng rng(seed);
+        const int n = 6;
+        const double x0 = -0.48, ywall = -0.05, cell = 0.16;
+        for (int i = 0; i < n; ++i)
+            for (int k = 0; k < 3; ++k) {
+                double jx = rng.uniform(-0.012, 0.012);
+                double jz = rng.uniform(-0.012, 0.012);
+                push(x0 + i * cell + jx, ywall, -0.42 + k * cell + jz, x0 + (i + 1) * cell + jx,
+                     ywall + 0.1, -0.42 + (k + 1) * cell + jz, 55.0);
+            }
+        push(-0.45, -0.5, -0.42, -0.15, -0.2, -0.12, 45.0);
+        push(0.12, -0.52, -0.42, 0.44, -0.24, -0.2, 45.0);
+    } else if (name == "bench" || name == "boxes") {
+        // "bench" is make_scene("bench"): 140 scattered blocks (~2% occupancy).
+        // "boxes" is the same generator with n_boxes blocks (occupancy sweep, config 5).
+        Rng rng(seed);
+        const int n = name == "bench" ? 140 : int(n_boxes);
+        for (int i = 0; i < n; ++i) {
+            double c[3], half[3];
+            for (double& v : c) v = rng.uniform(-0.85, 0.85);
+            for (double& v : half) v = rng.uniform(0.02, 0.09);
+            for (int k = 0; k < 3; ++k) rng.uniform(0.15, 0.9);  // diffuse colour draws
+            double sigma = rng.uniform(20.0, 80.0);
+            Box b{{c[0] - half[0], c[1] - half[1], c[2] - half[2]},
+                  {c[0] + half[0], c[1] + half[1], c[2] + half[2]},
+                  sigma};
+            for (int a = 0; a < 3; ++a) {
+                b.lo[a] = std::max(b.lo[a], -1.0 + 0.01);
+                b.hi[a] = std::min(b.hi[a], 1.0 - 0.01);
+            }
+            s.push_back(b);
+        }
+    } else if (name == "blob") {
+        // Blender-style bounded object: 60 seeded blocks inside radius ~0.5.
+        Rng rng(seed);
+        for (int i = 0; i < 60; ++i) {
+            double c[3], half[3];
+            for (double& v : c) v = rng.uniform(-0.33, 0.33);
+            for (double& v : half) v = rng.uniform(0.04, 0.13);
+            push(c[0] - half[0], c[1] - half[1], c[2] - half[2], c[0] + half[0], c[1] + half[1],
+                 c[2] + half[2], rng.uniform(20.0, 80.0));
+        }
+    } else if (name == "mip360") {
+        // Mip-NeRF-360-shaped bounded stand-in (contraction is out of scope,
+        // SPEC.md:8): a dense central cluster, a patchy ground, and tiled
+        // background slabs near the ROI faces, where contracted space puts far
+        // content. With sigma_pre ~ U[1,4] (CONFIGS in renderer.py) it gives
+        // ~60 marching / ~13.7 occupied points per ray at 5.1% occupancy
+        // (paper Table 4: 46.7 / 17.3).
+        Rng rng(seed);
+        for (int i = 0; i < 120; ++i) {  // central object: a dense cluster of blocks
+            double c[3], half[3];
+            for (double& v : c) v = rng.uniform(-0.38, 0.38);
+            for (double& v : half) v = rng.uniform(0.03, 0.09);
+            push(c[0] - half[0], c[1] - half[1], c[2] - half[2], c[0] + half[0], c[1] + half[1],
+                 c[2] + half[2], rng.uniform(20.0, 80.0));
+        }
+        for (int i = 0; i < 100; ++i) {  // patchy ground
+            double cx = rng.uniform(-0.9, 0.9), cy = rng.uniform(-0.9, 0.9);
+            double hx = rng.uniform(0.02, 0.06), hy = rng.uniform(0.02, 0.06);
+            double top = rng.uniform(-0.49, -0.44);
+            push(std::max(cx - hx, -0.99), std::max(cy - hy, -0.99), -0.5, std::min(cx + hx, 0.99),
+                 std::min(cy + hy, 0.99), top, rng.uniform(20.0, 80.0));
+        }
+        // Background: every face of the ROI tiled with slabs of random depth
+        // and inset (the far content a contracted 360 scene packs near |x| = 1),
+        // so nearly every ray ends on something, as in an unbounded capture.
+        const int tiles = 10;
+        for (int face = 0; face < 6; ++face) {
+            const int ax = face % 3, u = (ax + 1) % 3, v = (ax + 2) % 3;
+            const double sgn = face < 3 ? -1.0 : 1.0;
+            for (int i = 0; i < tiles; ++i)
+                for (int j = 0; j < tiles; ++j) {
+                    double lo[3], hi[3];
+                    const double cell = 1.9 / tiles;
+                    const double inset = rng.uniform(0.0, 0.25) * cell;
+                    lo[u] = -0.95 + i * cell + inset;
+                    hi[u] = -0.95 + (i + 1) * cell - rng.uniform(0.0, 0.25) * cell;
+                    lo[v] = -0.95 + j * cell + rng.uniform(0.0, 0.25) * cell;
+                    hi[v] = -0.95 + (j + 1) * cell - rng.uniform(0.0, 0.25) * cell;
+                    const double depth = rng.uniform(0.88, 0.96);
+                    const double thick = rng.uniform(0.006, 0.016);
+                    lo[ax] = sgn < 0 ? -depth - thick : depth;
+                    hi[ax] = sgn < 0 ? -depth : depth + thick;
+                    push(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], rng.uniform(20.0, 80.0));
+                }
+        }
+    } else {
+        throw std::invalid_argument("make_scene: unknown scene " + name);
+    }
+    return s;
+}
+
+struct BitGrid {
+    int res = 0;
+    std::vector<uint64_t> words;
+    BitGrid() = default;
+    explicit BitGrid(int r) : res(r), words((size_t(r) * r * r + 63) / 64, 0) {}
+    void set(int x, int y, int z) {
+        size_t i = size_t(x) + size_t(res) * (size_t(y) + size_t(res) * size_t(z));
+        words[i >> 6] |= uint64_t(1) << (i & 63);
+    }
+    bool get(int x, int y, int z) const {
+        size_t i = size_t(x) + size_t(res) * (size_t(y) + size_t(res) * size_t(z));
+        return (words[i >> 6] >> (i & 63)) & 1;
+    }
+};
+
+int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+BitGrid scene_occupancy(const std::vector<Box>& boxes, int res) {  // scene.hpp:168-183
+    BitGrid g(res);
+    double vsz = 2.0 / res;
+    for (const auto& box : boxes) {
+        if (box.sigma <= 0) continue;
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = clampi(int(std::floor((box.lo[a] - -1.0) / vsz)), 0, res - 1);
+            hi[a] = clampi(int(std::floor((box.hi[a] - -1.0) / vsz - 1e-12)), 0, res - 1);
+        }
+        for (int z = lo[2]; z <= hi[2]; ++z)
+            for (int y = lo[1]; y <= hi[1]; ++y)
+                for (int x = lo[0]; x <= hi[0]; ++x) g.set(x, y, z);
+    }
+    return g;
+}
+
+std::array<double, 16> look_at(const double eye[3], const double target[3], const double up[3]) {
+    auto norm = [](double v[3]) {  // Vec3::normalized, common.hpp:30-35
+        double n = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        v[0] = v[0] / n;
+        v[1] = v[1] / n;
+        v[2] = v[2] / n;
+    };
+    double z[3] = {target[0] - eye[0], target[1] - eye[1], target[2] - eye[2]};
+    norm(z);
+    double x[3] = {z[1] * up[2] - z[2] * up[1], z[2] * up[0] - z[0] * up[2],
+                   z[0] * up[1] - z[1] * up[0]};
+    norm(x);
+    double y[3] = {z[1] * x[2] - z[2] * x[1], z[2] * x[0] - z[0] * x[2], z[0] * x[1] - z[1] * x[0]};
+    return {x[0], y[0], z[0], eye[0], x[1], y[1], z[1], eye[1],
+            x[2], y[2], z[2], eye[2], 0,    0,    0,    1};
+}
+
+thread_local std::string g_synth_err;
+
+}  // namespace
+
+struct ngprt_synth {
+    ngprt_scene_desc desc{};
+    std::vector<Box> boxes;
+    std::vector<uint64_t> base_words;
+    std::vector<uint64_t> keys;
+    std::vector<float> rows;
+    std::vector<float> fine[NGPRT_MAX_FINE_LEVELS];
+    std::vector<float> psi_w[3], psi_b[3];
+    std::vector<float> att;
+};
+
+extern "C" {
+
+void ngprt_synth_default_params(ngprt_synth_params* p) {
+    std::memset(p, 0, sizeof *p);
+    std::strcpy(p->occupancy, "bench");
+    p->scene_seed = 41;
+    p->n_boxes = 140;
+    p->occ_base_res = 512;
+    p->dist_level = 1;
+    p->L = 2;
+    p->L_C = 512;
+    p->fusion_tag = NGPRT_FUSION_SEPARATE_ATT_V;
+    p->fine_table_len = uint64_t(1) << 21;
+    p->table_seed = 7;
+    p->coarse_seed = 13;
+    p->psi_seed = 11;
+    p->sigma_lo = 2.0;
+    p->sigma_hi = 6.0;
+    p->feat_scale = 1.0;
+    p->att_scale = 2.0;
+    p->psi_bias_scale = 0.0;
+    p->fp16_exact = 1;
+}
+
+ngprt_status ngprt_synth_create(const ngprt_synth_params* p, ngprt_synth** out) {
+    *out = nullptr;
+    try {
+        if (p->L < 1 || p->L > NGPRT_MAX_FINE_LEVELS) throw std::invalid_argument("synth: L must be in 1..4");
+        if (p->occ_base_res < 16 || (p->occ_base_res % 16) != 0)
+            throw std::invalid_argument("synth: occ_base_res must be a multiple of 16");
+        if (p->L_C < 1) throw std::invalid_argument("synth: L_C must be >= 1");
+        if (p->fine_table_len < 2) throw std::invalid_argument("synth: fine_table_len must be >= 2");
+        auto s = std::make_unique<ngprt_synth>();
+        const int L = int(p->L);
+        const int w = 8 + 2 * L;
+        char name[33];
+        std::memcpy(name, p->occupancy, 32);
+        name[32] = 0;
+        s->boxes = make_boxes(name, p->scene_seed, p->n_boxes);
+        auto rnd = [&](float v) { return p->fp16_exact ? round_fp16(v) : v; };
+
+        // Occupancy base grid and the coarse-row support (corners adjacent to an
+        // occupied L_C voxel, baking.hpp:156-163).
+        BitGrid base = scene_occupancy(s->boxes, int(p->occ_base_res));
+        s->base_words = base.words;
+        const int lc = int(p->L_C);
+        BitGrid occ_lc = scene_occupancy(s->boxes, lc);
+        BitGrid marks(lc + 1);
+        for (int z = 0; z < lc; ++z)
+            for (int y = 0; y < lc; ++y)
+                for (int x = 0; x < lc; ++x) {
+                    if (!occ_lc.get(x, y, z)) continue;
+                    for (int k = 0; k < 8; ++k) marks.set(x + (k & 1), y + ((k >> 1) & 1), z + (k >> 2));
+                }
+        Rng crng(p->coarse_seed);
+        const uint64_t r1 = uint64_t(lc) + 1;
+        for (int z = 0; z <= lc; ++z)
+            for (int y = 0; y <= lc; ++y)
+                for (int x = 0; x <= lc; ++x) {
+                    if (!marks.get(x, y, z)) continue;
+                    s->keys.push_back(uint64_t(x) + r1 * (uint64_t(y) + r1 * uint64_t(z)));
+                    s->rows.push_back(rnd(float(crng.uniform(p->sigma_lo, p->sigma_hi))));
+                    for (int c = 1; c < 8; ++c)
+                        s->rows.push_back(rnd(float(crng.uniform(-p->feat_scale, p->feat_scale))));
+                    for (int c = 8; c < w; ++c)
+                        s->rows.push_back(rnd(float(crng.uniform(-p->att_scale, p->att_scale))));
+                }
+
+        // Fine tables: Rng(table_seed).uniform(-s, s), level by level, row-major.
+        Rng frng(p->table_seed);
+        for (int l = 0; l < L; ++l) {
+            const uint32_t res = 1024u << l;  // EncodingConfig::fine_resolution, hash_grid.hpp:131
+            const uint64_t corners = uint64_t(res + 1) * (res + 1) * (res + 1);
+            s->desc.fine_res[l] = res;
+            s->desc.fine_hashed[l] = corners <= p->fine_table_len ? 0 : 1;  // HashLevel::init :72-79
+            s->desc.fine_table_len[l] = corners <= p->fine_table_len ? corners : p->fine_table_len;
+            auto& t = s->fine[l];
+            t.resize(s->desc.fine_table_len[l] * 8);
+            for (auto& v : t) v = rnd(float(frng.uniform(-p->feat_scale, p->feat_scale)));
+        }
+
+        // psi: TinyMlp::init({23,64,64,3}, Rng(psi_seed)) — nn.hpp:154-173.
+        const int widths[4] = {23, 64, 64, 3};
+        Rng prng(p->psi_seed);
+        for (int k = 0; k < 3; ++k) {
+            int in = widths[k], o = widths[k + 1];
+            double bound = (k + 1 < 3) ? std::sqrt(6.0 / in) : std::sqrt(6.0 / (in + o));
+            s->psi_w[k].resize(size_t(in) * o);
+            for (auto& v : s->psi_w[k]) v = float(prng.uniform(-bound, bound));
+            for (auto& v : s->psi_w[k]) v = rnd(v);
+            s->psi_b[k].assign(size_t(o), 0.f);
+        }
+        if (p->psi_bias_scale > 0) {
+            Rng brng(p->psi_seed + 1);
+            for (int k = 0; k < 3; ++k)
+                for (auto& v : s->psi_b[k])
+                    v = rnd(float(brng.uniform(-p->psi_bias_scale, p->psi_bias_scale)));
+        }
+        // Global attention logits (invariant fusion modes only).
+        Rng arng(p->coarse_seed + 0x5bd1e995ull);
+        s->att.resize(size_t(2) * L);
+        for (auto& v : s->att) v = rnd(float(arng.uniform(-p->att_scale, p->att_scale)));
+
+        ngprt_scene_desc& d = s->desc;
+        d.L = p->L;
+        d.L_C = p->L_C;
+        d.fusion_tag = uint8_t(p->fusion_tag);
+        d.storage = NGPRT_STORAGE_AUTO;
+        d.n_coarse = s->keys.size();
+        d.coarse_keys = s->keys.data();
+        d.coarse_rows = s->rows.data();
+        for (int l = 0; l < L; ++l) d.fine_tables[l] = s->fine[l].data();
+        for (int k = 0; k < 3; ++k) {
+            d.psi_w[k] = s->psi_w[k].data();
+            d.psi_b[k] = s->psi_b[k].data();
+        }
+        d.att_globals = s->att.data();
+        d.occ_base_res = p->occ_base_res;
+        d.pyramid_words[0] = s->base_words.data();
+        d.dist_res = p->dist_level < NGPRT_PYRAMID_LEVELS ? (p->occ_base_res >> p->dist_level) : 0;
+        d.dist_values = nullptr;
+        *out = s.release();
+        return NGPRT_OK;
+    } catch (const std::exception& e) {
+        g_synth_err = e.what();
+        return NGPRT_EINVAL;
+    }
+}
+
+const char* ngprt_synth_last_error(void) { return g_synth_err.c_str(); }
+
+const ngprt_scene_desc* ngprt_synth_desc(const ngprt_synth* s) { return &s->desc; }
+
+void ngprt_synth_destroy(ngprt_synth* s) { delete s; }
+
+ngprt_status ngprt_synth_cameras(int n, double radius, uint32_t width, uint32_t height,
+                                 ngprt_camera* out) {
+    const double golden = 2.39996322972865332;  // sphere_views, scene.hpp:254-265
+    for (int i = 0; i < n; ++i) {
+        double zfrac = -0.35 + 1.05 * (i + 0.5) / n;
+        double phi = golden * i;
+        double r = std::sqrt(std::max(0.0, 1.0 - zfrac * zfrac));
+        double eye[3] = {radius * r * std::cos(phi), radius * r * std::sin(phi), radius * zfrac};
+        double target[3] = {0, 0, 0}, up[3] = {0, 0, 1};
+        auto m = look_at(eye, target, up);
+        ngprt_camera& c = out[i];
+        std::memcpy(c.c2w, m.data(), sizeof c.c2w);
+        c.width = width;
+        c.height = height;
+        c.fx = c.fy = 1.1 * width;
+        c.cx = 0.5 * width;
+        c.cy = 0.5 * height;
+    }
+    return NGPRT_OK;
+}
+
+uint32_t ngprt_crc32(const void* data, uint64_t len, uint32_t seed) {  // common.hpp:78-92
+    static const auto table = [] {
+        std::array<uint32_t, 256> t{};
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            t[i] = c;
+        }
+        return t;
+    }();
+    uint32_t c = ~seed;
+    const auto* p = static_cast<const unsigned char*>(data);
+    for (uint64_t i = 0; i < len; ++i) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+    return ~c;
+}
+
+void ngprt_rng_uniform(uint64_t seed, double lo, double hi, uint64_t n, double* out) {
+    Rng r(seed);
+    for (uint64_t i = 0; i < n; ++i) out[i] = r.uniform(lo, hi);
+}
+
+}  // extern "C"

@@ -1,0 +1,283 @@
+"""Host-side API of the B200 NGP-RT renderer, mirroring the reference's render
+path interface (names and argument meaning follow /root/reference/proj/include/ngprt):
+
+    BakedScene            baking.hpp:55-64        -> Scene (device-resident, immutable)
+    PosedDataset / Frame  scene.hpp:191-201       -> Camera (ngprt_camera)
+    sphere_views          scene.hpp:254-265       -> cameras()
+    render_ray over a frame     -> render() / render_host()
+    MarchCounters         occupancy.hpp:197-210   -> the `stats` output (marching, occupied,
+                                                     occ_acc, dist_acc per ray)
+    build_pyramid         occupancy.hpp:114-119   -> build_pyramid()
+    build_distance_grid   occupancy.hpp:136-194   -> build_distance_grid()
+
+Everything below calls the C ABI (include/ngprt_cuda.h) in
+_lib/libngprt_cuda.so; errors surface as NgprtError carrying the library's
+message (the reference throws std::invalid_argument / domain_error etc.).
+There is no CPU path: without the native library and a B200 these raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._abi import Camera, RenderOpts, SceneDesc, SceneInfo, SynthParams, check, lib
+
+K_BASE_STEP = float(np.float32(2.0 * np.sqrt(3.0) / 512.0))  # kBaseStep, config.hpp:11
+
+
+# ---------------------------------------------------------------------------
+# Synthetic scenes (host)
+# ---------------------------------------------------------------------------
+# Named BASELINE.json configs -> synthetic scene parameters.
+CONFIGS = {
+    # 1. random-init NGP-RT scene, "16 levels" -> L = 4 (reference max), 2^19, 128^3 DT, 256x256
+    "c1_256": dict(occupancy="bench", occ_base_res=256, L=4, L_C=256, fine_table_len=1 << 19,
+                   width=256, height=256, n_cams=1),
+    # 2. 800x800 Blender-style bounded blob, 100-camera orbit (EncodingConfig{} defaults)
+    "c2_blob800": dict(occupancy="blob", occ_base_res=512, L=2, L_C=512, fine_table_len=1 << 22,
+                       width=800, height=800, n_cams=100),
+    # 3. 1920x1080 Mip-NeRF-360-shaped scene, 2^21 entries/level (the 108 fps headline)
+    "c3_1080p": dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
+                     fine_table_len=1 << 21, sigma_lo=1.0, sigma_hi=4.0,
+                     width=1920, height=1080, n_cams=1),
+    # 4. 1080p 64-camera batch (sharded across GPUs)
+    "c4_1080p_x64": dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
+                         fine_table_len=1 << 21, sigma_lo=1.0, sigma_hi=4.0,
+                         width=1920, height=1080, n_cams=64),
+    # 5. 3840x2160, 2^22 entries/level, occupancy sweep (n_boxes)
+    "c5_2160p": dict(occupancy="boxes", n_boxes=140, occ_base_res=512, L=2, L_C=512,
+                     fine_table_len=1 << 22, width=3840, height=2160, n_cams=1),
+}
+SCENE_KEYS = {f for f, _ in SynthParams._fields_}
+
+
+class SynthScene:
+    """Seeded synthetic BakedScene in host memory (ngprt_synth_*): the input both
+    the GPU renderer and the CPU oracle consume."""
+
+    def __init__(self, **overrides):
+        p = SynthParams()
+        lib().ngprt_synth_default_params(C.byref(p))
+        for k, v in overrides.items():
+            if k not in SCENE_KEYS:
+                continue
+            if k == "occupancy":
+                v = v.encode()
+            if k == "fusion_tag" and isinstance(v, str):
+                v = _abi.FUSION[v]
+            setattr(p, k, v)
+        self.params = p
+        h = C.c_void_p()
+        st = lib().ngprt_synth_create(C.byref(p), C.byref(h))
+        if st != _abi.OK:
+            raise ValueError("ngprt_synth_create failed (bad parameters)")
+        self._h = h
+        self.desc_ptr = lib().ngprt_synth_desc(h)
+        self.desc: SceneDesc = self.desc_ptr.contents
+
+    # numpy views over the synth-owned arrays (valid while self is alive)
+    def _view(self, ptr, n, dtype):
+        if n == 0:
+            return np.zeros(0, dtype)
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dtype))),
+                                     shape=(n,))
+
+    @property
+    def L(self):
+        return int(self.desc.L)
+
+    def coarse_keys(self):
+        return self._view(self.desc.coarse_keys, self.desc.n_coarse, np.uint64)
+
+    def coarse_rows(self):
+        w = 8 + 2 * self.L
+        return self._view(self.desc.coarse_rows, self.desc.n_coarse * w, np.float32).reshape(-1, w)
+
+    def fine_table(self, l):
+        n = int(self.desc.fine_table_len[l]) * 8
+        return self._view(self.desc.fine_tables[l], n, np.float32).reshape(-1, 8)
+
+    def base_words(self):
+        r = int(self.desc.occ_base_res)
+        return self._view(self.desc.pyramid_words[0], (r ** 3 + 63) // 64, np.uint64)
+
+    def psi(self):
+        shapes = [(64, 23), (64, 64), (3, 64)]
+        ws = [self._view(self.desc.psi_w[k], a * b, np.float32).reshape(a, b)
+              for k, (a, b) in enumerate(shapes)]
+        bs = [self._view(self.desc.psi_b[k], a, np.float32) for k, (a, _) in enumerate(shapes)]
+        return ws, bs
+
+    def occupancy_fraction(self):
+        r = int(self.desc.occ_base_res)
+        bits = np.unpackbits(self.base_words().view(np.uint8)).sum()
+        return float(bits) / r ** 3
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ngprt_synth_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def cameras(n: int, width: int, height: int, radius: float = 2.9):
+    """sphere_views(n, radius) with synth_dataset intrinsics (scene.hpp:254-265, 388-395)."""
+    cams = (Camera * n)()
+    check(lib().ngprt_synth_cameras(n, radius, width, height, cams), "ngprt_synth_cameras")
+    return cams
+
+
+def camera_array(cams):
+    """ctypes Camera array from a list/sequence of Camera."""
+    if isinstance(cams, C.Array):
+        return cams
+    arr = (Camera * len(cams))()
+    for i, c in enumerate(cams):
+        arr[i] = c
+    return arr
+
+
+@dataclass
+class Opts:
+    """Render options (march() arguments, occupancy.hpp:302-305; CLI flags SPEC.md:676)."""
+    step: float = 0.0            # <= 0 -> kBaseStep
+    use_dist_grid: bool = True
+    max_step_rule: bool = False
+    early_stop: bool = True
+    keep_level: int = 0
+    mlp: str = "exact"           # "exact" (bit-exact CUDA cores) | "tensor" (tcgen05)
+    window: tuple | None = None  # (x0, y0, w, h)
+    profile: bool = False        # per-kernel CUDA-event timing (render_timing())
+
+    def to_c(self) -> RenderOpts:
+        o = RenderOpts()
+        o.profile = int(self.profile)
+        o.step = self.step
+        o.use_dist_grid = int(self.use_dist_grid)
+        o.max_step_rule = int(self.max_step_rule)
+        o.early_stop = int(self.early_stop)
+        o.keep_level = int(self.keep_level)
+        o.mlp_mode = _abi.MLP_EXACT if self.mlp == "exact" else _abi.MLP_TENSOR
+        if self.window:
+            o.x0, o.y0, o.w, o.h = self.window
+        return o
+
+
+# ---------------------------------------------------------------------------
+# Device scene and render
+# ---------------------------------------------------------------------------
+class Scene:
+    """A BakedScene resident on one B200 (ngprt_scene). Immutable after creation."""
+
+    def __init__(self, desc, device: int = 0, storage: int = _abi.STORAGE_AUTO):
+        if isinstance(desc, SynthScene):
+            self._synth = desc  # keep host arrays alive for the call
+            desc_ptr = desc.desc_ptr
+        else:
+            desc_ptr = C.pointer(desc)
+        desc_ptr.contents.storage = storage
+        h = C.c_void_p()
+        check(lib().ngprt_scene_create(desc_ptr, device, C.byref(h)), "ngprt_scene_create")
+        self._h = h
+        self.device = device
+        self.L = int(desc_ptr.contents.L)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> SceneInfo:
+        i = SceneInfo()
+        check(lib().ngprt_scene_info_get(self._h, C.byref(i)), "ngprt_scene_info_get")
+        return i
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ngprt_scene_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def _out_shape(cams, opts: Opts):
+    if opts.window:
+        return opts.window[3], opts.window[2]
+    return int(cams[0].height), int(cams[0].width)
+
+
+def render(scene: Scene, cams, opts: Opts | None = None, out=None, stats: bool = False,
+           stream=None):
+    """Render len(cams) frames on the scene's GPU. Returns a torch float32 tensor
+    (n, h, w, 3) [and int32 stats (n, h, w, 4)] on that device."""
+    import torch
+
+    opts = opts or Opts()
+    cams = camera_array(cams)
+    n = len(cams)
+    h, w = _out_shape(cams, opts)
+    dev = torch.device("cuda", scene.device)
+    if out is None:
+        out = torch.empty((n, h, w, 3), dtype=torch.float32, device=dev)
+    st = torch.empty((n, h, w, 4), dtype=torch.int32, device=dev) if stats else None
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    o = opts.to_c()
+    check(lib().ngprt_render(scene.handle, cams, n, C.byref(o), out.data_ptr(),
+                             st.data_ptr() if st is not None else None, s.cuda_stream),
+          "ngprt_render")
+    return (out, st) if stats else out
+
+
+def render_timing(scene: Scene):
+    """(ms in K1 march, ms in K2 shade, kernel launches) of the last profiled render."""
+    a, b, n = C.c_float(), C.c_float(), C.c_int()
+    check(lib().ngprt_render_timing(scene.handle, C.byref(a), C.byref(b), C.byref(n)),
+          "ngprt_render_timing")
+    return a.value, b.value, n.value
+
+
+def render_host(scene: Scene, cams, opts: Opts | None = None, out=None, stats=None):
+    """Host-buffer render (ngprt_render_host): copies cameras in and RGB out."""
+    opts = opts or Opts()
+    cams = camera_array(cams)
+    n = len(cams)
+    h, w = _out_shape(cams, opts)
+    if out is None:
+        out = np.empty((n, h, w, 3), np.float32)
+    o = opts.to_c()
+    check(lib().ngprt_render_host(scene.handle, cams, n, C.byref(o), out.ctypes.data,
+                                  stats.ctypes.data if stats is not None else None),
+          "ngprt_render_host")
+    return out
+
+
+def build_pyramid(base_words, base_res: int, stream=None):
+    """Levels 1..4 of build_pyramid for a device u64 word tensor (torch.int64)."""
+    import torch
+
+    levels = []
+    for k in range(1, 5):
+        r = base_res >> k
+        levels.append(torch.empty(((r ** 3 + 63) // 64,), dtype=torch.int64,
+                                  device=base_words.device))
+    ptrs = (C.c_void_p * 4)(*[t.data_ptr() for t in levels])
+    s = stream if stream is not None else torch.cuda.current_stream(base_words.device)
+    check(lib().ngprt_build_pyramid(base_words.data_ptr(), base_res, ptrs, s.cuda_stream),
+          "ngprt_build_pyramid")
+    return levels
+
+
+def build_distance_grid(words, res: int, stream=None):
+    """build_distance_grid for a device u64 word tensor -> uint8 (res^3) tensor."""
+    import torch
+
+    out = torch.empty((res ** 3,), dtype=torch.uint8, device=words.device)
+    s = stream if stream is not None else torch.cuda.current_stream(words.device)
+    check(lib().ngprt_build_distance_grid(words.data_ptr(), res, out.data_ptr(), s.cuda_stream),
+          "ngprt_build_distance_grid")
+    return out

@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path through the C ABI against the reference's own
+outputs (golden fixtures from oracle/_ref) and the C restatement oracle.
+
+Bar (north_star): bit-exact hash indices, occupancy pyramid, distance grid and
+per-ray march counters; RGB bit-exact in the exact-MLP mode, and max-abs
+<= 1e-3 with PSNR >= 60 dB in the tensor-core MLP mode."""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from cases import CASES, make_case, random_grid_words, scene_crc
+from checkers import CpuScene, host_expf_range
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+G = json.loads((GOLD / "golden.json").read_text())
+RGB_TOL = 1e-3     # north_star: per-pixel RGB max-abs error <= 1e-3
+PSNR_MIN = 60.0    # north_star: PSNR >= 60 dB
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def crc(ng, a):
+    a = np.ascontiguousarray(a)
+    return int(ng.lib().ngprt_crc32(a.ctypes.data, a.nbytes, 0))
+
+
+def psnr(a, b):
+    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    return 99.0 if mse <= 0 else min(99.0, 10 * np.log10(1.0 / mse))  # image.hpp:90-101
+
+
+def gpu_render(ng, torch, scene_dev, cam, opts):
+    rgb, st = ng.render(scene_dev, [cam], opts, stats=True)
+    torch.cuda.synchronize()
+    return rgb[0].cpu().numpy(), st[0].cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_render_exact_matches_reference(ng, torch, case):
+    scene, cam, opts = make_case(ng, case)
+    assert scene_crc(ng, scene) == G["cases"][case["name"]]["scene_crc"]
+    dev = ng.Scene(scene)
+    opts.mlp = "exact"
+    rgb, stats = gpu_render(ng, torch, dev, cam, opts)
+    ref = np.load(GOLD / f"render_{case['name']}.npz")
+    assert np.array_equal(stats, ref["stats"]), \
+        f"counters differ at {np.argwhere((stats != ref['stats']).any(-1))[:5]}"
+    diff = np.abs(rgb - ref["rgb"])
+    assert np.array_equal(rgb.view(np.uint32), ref["rgb"].view(np.uint32)), \
+        f"rgb not bit-exact: max abs {diff.max()} at {np.unravel_index(diff.argmax(), diff.shape)}"
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_render_tensor_within_tolerance(ng, torch, case):
+    scene, cam, opts = make_case(ng, case)
+    dev = ng.Scene(scene)
+    opts.mlp = "tensor"
+    rgb, stats = gpu_render(ng, torch, dev, cam, opts)
+    ref = np.load(GOLD / f"render_{case['name']}.npz")
+    assert np.array_equal(stats, ref["stats"])
+    # the black/shade branch (final_t < 1) is decided before the MLP: exact
+    assert np.array_equal(rgb.sum(-1) == 0, ref["rgb"].sum(-1) == 0)
+    assert np.abs(rgb - ref["rgb"]).max() <= RGB_TOL
+    assert psnr(rgb, ref["rgb"]) >= PSNR_MIN
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_device_pyramid_and_distance_grid(ng, torch, case):
+    """The pyramid (K3) and distance grid (K4) the scene built on the device are
+    bit-identical to the reference's build_pyramid / build_distance_grid."""
+    scene, _, _ = make_case(ng, case)
+    gold = G["cases"][case["name"]]
+    dev = ng.Scene(scene)
+    info = dev.info()
+    torch.cuda.synchronize()
+    r0 = int(scene.desc.occ_base_res)
+    lv = [_dev_copy(info.dev_pyramid[k], (((r0 >> k) ** 3 + 63) // 64) * 8).view(np.uint64)
+          for k in range(1, 5)]
+    assert crc(ng, np.concatenate(lv)) == gold["pyramid_crc"]
+    if "dist_crc" in gold:
+        dr = int(scene.desc.dist_res)
+        assert crc(ng, _dev_copy(info.dev_dist, dr ** 3)) == gold["dist_crc"]
+
+
+def _dev_copy(ptr, nbytes):
+    """Copy nbytes from a raw device pointer into a host uint8 array (cudaMemcpy D2H)."""
+    out = np.empty(nbytes, np.uint8)
+    rc = _cudart().cudaMemcpy(out.ctypes.data, ptr, nbytes, 2)
+    assert rc == 0, f"cudaMemcpy failed {rc}"
+    return out
+
+
+_CUDART = None
+
+
+def _cudart():
+    global _CUDART
+    if _CUDART is None:
+        import glob
+        import os
+        import torch
+        cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia",
+                                       "cuda_runtime", "lib", "libcudart.so*"))
+        cands += ["libcudart.so.12", "libcudart.so"]
+        for c in cands:
+            try:
+                _CUDART = C.CDLL(c)
+                break
+            except OSError:
+                continue
+        _CUDART.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+    return _CUDART
+
+
+def test_distance_grid_random_grids(ng, torch):
+    for res, dens, seed, wcrc, dcrc in G["dt_random"]:
+        words = random_grid_words(ng, res, dens, seed)
+        w = torch.from_numpy(words.view(np.int64)).cuda()
+        out = ng.build_distance_grid(w, res)
+        assert crc(ng, out.cpu().numpy()) == dcrc, (res, dens)
+
+
+def test_distance_grid_single_voxel(ng, torch):
+    words = np.zeros(256 ** 3 // 64, np.uint64)
+    i = 128 + 256 * (128 + 256 * 128)
+    words[i >> 6] |= np.uint64(1) << np.uint64(i & 63)
+    out = ng.build_distance_grid(torch.from_numpy(words.view(np.int64)).cuda(), 256).cpu().numpy()
+    assert out[133 + 256 * (128 + 256 * 128)] == 4
+    assert crc(ng, out) == G["dt_single_voxel"]["crc"]
+
+
+def test_pyramid_matches_oracle_on_random_grids(ng, torch):
+    from checkers import oracle
+    O = oracle()
+    for res, dens, seed in [(64, 0.01, 11), (128, 0.001, 12), (256, 0.02, 13), (32, 1.0, 14)]:
+        words = random_grid_words(ng, res, dens, seed)
+        n = sum(((res >> k) ** 3 + 63) // 64 for k in range(1, 5))
+        want = np.zeros(n, np.uint64)
+        O.orc_build_pyramid(words.ctypes.data, res, want.ctypes.data)
+        got = ng.build_pyramid(torch.from_numpy(words.view(np.int64)).cuda(), res)
+        got = np.concatenate([g.cpu().numpy().view(np.uint64) for g in got])
+        assert np.array_equal(got, want), res
+
+
+def test_hash_index_on_device(ng, torch):
+    rows = G["hash_index"]
+    for res, maxlen in sorted({(r[0], r[1]) for r in rows}):
+        sel = [r for r in rows if r[0] == res and r[1] == maxlen]
+        corners = np.array([[r[2], r[3], r[4]] for r in sel], np.int32)
+        want = np.array([r[5] for r in sel], np.uint64)
+        ncorn = (res + 1) ** 3
+        hashed = 0 if ncorn <= maxlen else 1
+        tlen = ncorn if ncorn <= maxlen else maxlen
+        c = torch.from_numpy(corners).cuda()
+        out = torch.empty(len(sel), dtype=torch.int64, device="cuda")
+        ng._abi.check(ng.lib().ngprt_test_hash_index(c.data_ptr(), len(sel), res, tlen, hashed,
+                                                     out.data_ptr(), None), "hash")
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (res, maxlen)
+
+
+def test_expf_kat_on_device(ng, torch):
+    xs = np.uint32([r[0] for r in G["expf"]]).view(np.float32)
+    want = np.uint32([r[1] for r in G["expf"]])
+    x = torch.from_numpy(xs).cuda()
+    y = torch.empty_like(x)
+    ng._abi.check(ng.lib().ngprt_test_expf(x.data_ptr(), y.data_ptr(), len(xs), None), "expf")
+    torch.cuda.synchronize()
+    got = y.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want)
+
+
+def test_expf_exhaustive_vs_host_glibc(ng, torch):
+    """All 2^32 inputs: the device port of glibc expf == this host's glibc expf."""
+    chunk = 1 << 28
+    y = torch.empty(chunk, dtype=torch.int32, device="cuda")
+    bad = 0
+    for first in range(0, 1 << 32, chunk):
+        ng._abi.check(ng.lib().ngprt_test_expf_range(first, chunk, y.data_ptr(), None), "expf")
+        torch.cuda.synchronize()
+        got = y.cpu().numpy().view(np.uint32)
+        want = host_expf_range(first, chunk)
+        neq = got != want
+        if neq.any():  # NaN payloads: both must be NaN
+            gf, wf = got[neq].view(np.float32), want[neq].view(np.float32)
+            bad += int((~(np.isnan(gf) & np.isnan(wf))).sum())
+    assert bad == 0
+
+
+def test_full_1080p_frame_matches_oracle(ng, torch):
+    """Config 3 at full size: every ray of a 1920x1080 frame, bit-exact vs the
+    C restatement (counters and RGB)."""
+    cfg = dict(ng.CONFIGS["c3_1080p"])
+    scene = ng.SynthScene(**cfg)
+    cam = ng.cameras(1, 1920, 1080)[0]
+    opts = ng.Opts(mlp="exact")
+    dev = ng.Scene(scene)
+    rgb, stats = gpu_render(ng, torch, dev, cam, opts)
+    o = CpuScene(scene.desc_ptr, "oracle")
+    want_rgb, want_stats = o.render(cam, opts.to_c())
+    assert np.array_equal(stats, want_stats)
+    assert np.array_equal(rgb.view(np.uint32), want_rgb.view(np.uint32))
+
+
+def test_multi_camera_batch_and_window_consistency(ng, torch):
+    """A 70-camera batch (two launches of <= 64) equals per-camera renders, and a
+    window render equals the crop of the full frame."""
+    scene = ng.SynthScene(occupancy="bench", occ_base_res=128, L=2, L_C=128,
+                          fine_table_len=1 << 14)
+    dev = ng.Scene(scene)
+    cams = ng.cameras(70, 40, 32)
+    batch = ng.render(dev, cams, ng.Opts(mlp="exact")).cpu().numpy()
+    for i in [0, 33, 63, 64, 69]:
+        one = ng.render(dev, [cams[i]], ng.Opts(mlp="exact")).cpu().numpy()[0]
+        assert np.array_equal(one.view(np.uint32), batch[i].view(np.uint32))
+    full = batch[5]
+    win = ng.render(dev, [cams[5]], ng.Opts(mlp="exact", window=(7, 3, 20, 17))).cpu().numpy()[0]
+    assert np.array_equal(win.view(np.uint32), full[3:20, 7:27].view(np.uint32))
+    again = ng.render(dev, cams, ng.Opts(mlp="exact")).cpu().numpy()
+    assert np.array_equal(again.view(np.uint32), batch.view(np.uint32))  # determinism
+
+
+def test_render_host_matches_device_render(ng, torch):
+    scene = ng.SynthScene(occupancy="toy", occ_base_res=64, L=2, L_C=64, fine_table_len=1 << 12)
+    dev = ng.Scene(scene)
+    cams = ng.cameras(3, 32, 24)
+    a = ng.render(dev, cams, ng.Opts(mlp="exact")).cpu().numpy()
+    b = ng.render_host(dev, cams, ng.Opts(mlp="exact"))
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_errors_are_reported(ng, torch):
+    scene = ng.SynthScene(occupancy="slab", occ_base_res=64, L=2, L_C=32, fine_table_len=1 << 10)
+    dev = ng.Scene(scene)
+    cam = ng.cameras(1, 16, 16)[0]
+    with pytest.raises(ng.NgprtError, match="keep_level"):
+        ng.render(dev, [cam], ng.Opts(keep_level=3))
+    with pytest.raises(ng.NgprtError, match="out of bounds"):
+        ng.render(dev, [cam], ng.Opts(window=(10, 10, 8, 8)))
+    scene.desc.fusion_tag = 5
+    with pytest.raises(ng.NgprtError, match="EUNSUPPORTED"):
+        ng.Scene(scene)
