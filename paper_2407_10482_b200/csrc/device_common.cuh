@@ -123,6 +123,23 @@ struct DevScene {
     int dist_res;
     const uint8_t* dist;
     const float* psi;     // packed f32 weights: W0 (64x23) b0 W1 (64x64) b1 W2 (3x64) b2
+
+    // ---- derived constants (ngprt_scene_create); each equals the float the
+    // reference computes at that point, so using them is bit-exact ----
+    float occ_h0;                                   // float(r0)/2.0f (to_grid_coord scale)
+    float lvl_two_over_res[NGPRT_PYRAMID_LEVELS];   // 2.0f/float(r_k)  (voxel_exit_step hi)
+    float lvl_inv_res[NGPRT_PYRAMID_LEVELS];        // 1/r_k, exact when r_k is a power of two
+    int occ_pow2;                                   // every r_k is a power of two
+    // Probe code per level-1 voxel (r1^3 u16): bits 8..10 = e, the number of
+    // pyramid levels 4..1 whose bit is set before the first clear one (e = 4:
+    // all set, level 0 decides); bits 0..7 = distance value G when dist_res == r1.
+    const uint16_t* probe;
+    int dist_is_l1;                                 // dist_res == r1
+    float dist_h;                                   // float(dist_res)/2.0f
+    float dist_vox;                                 // float(2.0/dist_res) (DistanceGrid::voxel_size)
+    float coarse_h;                                 // float(L_C)/2.0f
+    float fine_h[NGPRT_MAX_FINE_LEVELS];            // float(fine_res[l])/2.0f
+    int coarse_u32;                                 // (L_C+1)^3 < 2^32: 32-bit corner keys
 };
 
 constexpr int kPsiW0 = 0, kPsiB0 = 64 * 23, kPsiW1 = kPsiB0 + 64, kPsiB1 = kPsiW1 + 64 * 64,

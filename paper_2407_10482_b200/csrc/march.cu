@@ -1,15 +1,30 @@
 // march.cu — K1: ray generation, empty-space-skipping march, per-sample gather
 // of baked coarse rows and fine hash features, attention fusion and
-// front-to-back compositing with early stop. One thread per ray, 16x8 pixel
-// tiles per 128-thread CTA.
+// front-to-back compositing with early stop.
 //
-// Built with -fmad=false: every float/double expression below rounds exactly
-// where the reference's does. Reference citations are
-// relative to /root/reference/proj/include/ngprt/.
+// Execution model: persistent warps, one ray per lane. Rays come in 8x4 pixel
+// tiles from a global counter; a lane whose ray finishes is refilled from the
+// warp's current tile. Lanes march independently, but a lane that reaches an
+// occupied point parks there until enough lanes of the warp are parked
+// (kDecodeMin) or no lane can step: the expensive sample decode then runs
+// with most lanes converged instead of serialising against cheap empty steps.
+//
+// Parity: built with -fmad=false and every float/double operation is the
+// reference's, in its order. Two restructurings are
+// exact by construction and documented inline: (1) pyramid voxel indices at
+// level k are the level-0 index >> k (power-of-two scaling commutes with
+// rounding), (2) division by a power-of-two resolution is multiplication by
+// its exact reciprocal. Reference citations are relative to
+// /root/reference/proj/include/ngprt/.
 #include "render.cuh"
 
 namespace ngprt_dev {
 namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kDecodeMin = 12;  // parked lanes that trigger a warp-wide decode
+constexpr int kStepBurst = 4;   // marching points a stepping lane takes per round
+constexpr int kMinBlocks = 5;   // register budget: 65536 / (128 * 5) = 102 regs
 
 struct Ray {
     float o[3], d[3];
@@ -30,7 +45,6 @@ __device__ __forceinline__ bool generate_ray(const CamParams& c, double u, doubl
     w[2] = w[2] / n;
     const double o[3] = {c.m[3], c.m[7], c.m[11]};
     double t0 = 0.0, t1 = 1e9;
-#pragma unroll
     for (int a = 0; a < 3; ++a) {
         if (w[a] == 0.0) {
             if (o[a] < -1.0 || o[a] > 1.0) return false;
@@ -46,7 +60,6 @@ __device__ __forceinline__ bool generate_ray(const CamParams& c, double u, doubl
         t1 = (tb < t1) ? tb : t1;
     }
     if (!(t0 < t1)) return false;
-#pragma unroll
     for (int a = 0; a < 3; ++a) {
         r.o[a] = float(o[a]);
         r.d[a] = float(w[a]);
@@ -79,46 +92,16 @@ __device__ __forceinline__ bool clip_f(const Ray& r, float& t0, float& t1) {
     return t0 < t1;
 }
 
-// to_grid_coord hash_grid.hpp:23-26; voxel_of occupancy.hpp:94-102
-__device__ __forceinline__ float grid_coord(float x, int res) {
-    return (x - (-1.0f)) * (float(res) / 2.0f);
-}
-__device__ __forceinline__ int voxel_1d(float x, int res) {
-    int i = int(floorf(grid_coord(x, res)));
+// voxel_of along one axis (occupancy.hpp:94-102) with h = float(res)/2.0f,
+// i.e. to_grid_coord (hash_grid.hpp:23-26) then floor and clamp.
+__device__ __forceinline__ int voxel_1d(float x, float h, int res) {
+    const int i = int(floorf((x - (-1.0f)) * h));
     return i < 0 ? 0 : (i > res - 1 ? res - 1 : i);
 }
 
-__device__ __forceinline__ bool occ_bit(const uint32_t* __restrict__ g, int res, int x, int y,
-                                        int z) {
-    const unsigned long long i =
-        (unsigned long long)x + (unsigned long long)res * ((unsigned long long)y +
-                                                           (unsigned long long)res * z);
-    return (__ldg(g + (i >> 5)) >> (uint32_t(i) & 31u)) & 1u;
-}
-
-// voxel_exit_step, occupancy.hpp:238-255 (x = ray.at(t), not clamped)
-__device__ __forceinline__ float voxel_exit_step(const Ray& r, float t, int res) {
-    float t_exit = 3.402823466e38f;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const float d = r.d[a];
-        if (d == 0.0f) continue;
-        const float xa = r.o[a] + d * t;
-        const int v = voxel_1d(xa, res);
-        const float lo = -1.0f + 2.0f * float(v) / float(res);
-        const float hi = lo + 2.0f / float(res);
-        const float bound = d > 0.0f ? hi : lo;
-        const float tc = (bound - r.o[a]) / d;
-        t_exit = (tc < t_exit) ? tc : t_exit;
-    }
-    float s = t_exit - t;
-    if (!(s > 0.0f)) s = 0.0f;
-    return s + 1e-6f;
-}
-
 // Stencil along one axis: base index and fractional offset (hash_grid.hpp:38-46).
-__device__ __forceinline__ void stencil_axis(float x, int res, int& base, float& frac) {
-    const float u = grid_coord(x, res);
+__device__ __forceinline__ void stencil_axis(float x, float h, int res, int& base, float& frac) {
+    const float u = (x - (-1.0f)) * h;
     int i = int(floorf(u));
     i = i < res - 1 ? i : res - 1;
     i = i > 0 ? i : 0;
@@ -126,7 +109,7 @@ __device__ __forceinline__ void stencil_axis(float x, int res, int& base, float&
     frac = u - float(i);
 }
 
-// Row loads: N leading elements of a row, converted to f32 (exact).
+// Row loads: N leading elements of a 16-element row, converted to f32 (exact).
 template <int N, bool F16>
 __device__ __forceinline__ void load_coarse_row(const void* __restrict__ base,
                                                 unsigned long long row, float* out) {
@@ -140,8 +123,17 @@ __device__ __forceinline__ void load_coarse_row(const void* __restrict__ base,
             out[2 * i] = f.x;
             out[2 * i + 1] = f.y;
         }
-        if constexpr (N > 8) {
+        if constexpr (N > 12) {
             const uint4 b = __ldg(p + 1);
+            const __half2* hb = reinterpret_cast<const __half2*>(&b);
+#pragma unroll
+            for (int i = 0; i < (N - 8) / 2; ++i) {
+                const float2 f = __half22float2(hb[i]);
+                out[8 + 2 * i] = f.x;
+                out[9 + 2 * i] = f.y;
+            }
+        } else if constexpr (N > 8) {
+            const uint2 b = __ldg(reinterpret_cast<const uint2*>(p + 1));
             const __half2* hb = reinterpret_cast<const __half2*>(&b);
 #pragma unroll
             for (int i = 0; i < (N - 8) / 2; ++i) {
@@ -201,6 +193,18 @@ __device__ __forceinline__ unsigned long long fine_index(const DevScene& sc, int
     return (unsigned long long)x + r1 * ((unsigned long long)y + r1 * (unsigned long long)z);
 }
 
+// Trilinear weights in corner order k (bit0 x, bit1 y, bit2 z): w_k = (wx*wy)*wz
+// (hash_grid.hpp:50-54); the wx*wy products are shared, the values are identical.
+__device__ __forceinline__ void corner_weights(const float f[3], float w[8]) {
+    const float wx[2] = {1.0f - f[0], f[0]}, wy[2] = {1.0f - f[1], f[1]},
+                wz[2] = {1.0f - f[2], f[2]};
+    float wxy[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) wxy[j] = wx[j & 1] * wy[j >> 1];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = wxy[k & 3] * wz[k >> 2];
+}
+
 // decode_point_baked (baking.hpp:68-91) + split_decoder_output (model.hpp:13-22)
 // + level_masked_fine (fusion.hpp:198-209) + fuse (fusion.hpp:107-173).
 template <int L, bool F16>
@@ -214,28 +218,38 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
         int cb[3];
         float cf[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.L_C, cb[a], cf[a]);
-        const unsigned long long r1 = (unsigned long long)sc.L_C + 1;
-        float rows[8][W];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const unsigned long long key =
-                (unsigned long long)(cb[0] + (k & 1)) +
-                r1 * ((unsigned long long)(cb[1] + ((k >> 1) & 1)) +
-                      r1 * (unsigned long long)(cb[2] + (k >> 2)));
-            load_coarse_row<W, F16>(sc.coarse, key, rows[k]);
-        }
+        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.coarse_h, sc.L_C, cb[a], cf[a]);
+        float w[8];
+        corner_weights(cf, w);
+        const uint32_t r1 = uint32_t(sc.L_C) + 1;
 #pragma unroll
         for (int i = 0; i < W; ++i) dec[i] = 0.0f;
+        if (sc.coarse_u32) {
+            const uint32_t key0 = uint32_t(cb[0]) + r1 * (uint32_t(cb[1]) + r1 * uint32_t(cb[2]));
+            const uint32_t sy = r1, sz = r1 * r1;
+            float rows[8][W];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-            const float wx = dx ? cf[0] : 1.0f - cf[0];
-            const float wy = dy ? cf[1] : 1.0f - cf[1];
-            const float wz = dz ? cf[2] : 1.0f - cf[2];
-            const float wk = wx * wy * wz;
+            for (int k = 0; k < 8; ++k)
+                load_coarse_row<W, F16>(sc.coarse,
+                                        key0 + (k & 1) + ((k >> 1) & 1) * sy + (k >> 2) * sz,
+                                        rows[k]);
 #pragma unroll
-            for (int i = 0; i < W; ++i) dec[i] += wk * rows[k][i];
+            for (int k = 0; k < 8; ++k)
+#pragma unroll
+                for (int i = 0; i < W; ++i) dec[i] += w[k] * rows[k][i];
+        } else {
+            const unsigned long long R1 = r1;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const unsigned long long key =
+                    (unsigned long long)(cb[0] + (k & 1)) +
+                    R1 * ((unsigned long long)(cb[1] + ((k >> 1) & 1)) +
+                          R1 * (unsigned long long)(cb[2] + (k >> 2)));
+                float row[W];
+                load_coarse_row<W, F16>(sc.coarse, key, row);
+#pragma unroll
+                for (int i = 0; i < W; ++i) dec[i] += w[k] * row[i];
+            }
         }
     }
     // fine levels: stencil, hash, 8 rows, interpolation (hash_grid.hpp:97-106)
@@ -245,26 +259,30 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
         int b[3];
         float f[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_res[l], b[a], f[a]);
+        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[l], sc.fine_res[l], b[a], f[a]);
+        float w[8];
+        corner_weights(f, w);
+        unsigned long long idx[8];
+        if (sc.fine_mode[l] == 1) {
+            const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
+            const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                idx[k] = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & sc.fine_mask[l];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                idx[k] = fine_index(sc, l, b[0] + (k & 1), b[1] + ((k >> 1) & 1), b[2] + (k >> 2));
+        }
         float frow[8][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-            const unsigned long long idx = fine_index(sc, l, b[0] + dx, b[1] + dy, b[2] + dz);
-            load_fine_row<F16>(sc.fine[l], idx, frow[k]);
-        }
+        for (int k = 0; k < 8; ++k) load_fine_row<F16>(sc.fine[l], idx[k], frow[k]);
 #pragma unroll
         for (int c = 0; c < 8; ++c) fine[l][c] = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-            const float wx = dx ? f[0] : 1.0f - f[0];
-            const float wy = dy ? f[1] : 1.0f - f[1];
-            const float wz = dz ? f[2] : 1.0f - f[2];
-            const float wk = wx * wy * wz;
+        for (int k = 0; k < 8; ++k)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) fine[l][c] += wk * frow[k][c];
-        }
+            for (int c = 0; c < 8; ++c) fine[l][c] += w[k] * frow[k][c];
     }
     if (keep_level > 0) {
 #pragma unroll
@@ -302,107 +320,261 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
     }
 }
 
+// Per-lane ray state.
+struct Lane {
+    Ray ray;
+    float t, t1;
+    float xc[3];  // clamped sample position of a parked (pending) lane
+    float cd[3], fs[4], T;
+    uint32_t n_march, n_occ, n_occ_acc, n_dist;
+    uint32_t out_idx;
+    bool has_ray, pending;
+};
+
+__device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s, bool valid) {
+    RayAcc r;
+    r.a = make_float4(s.cd[0], s.cd[1], s.cd[2], s.T);
+    r.b = make_float4(s.fs[0], s.fs[1], s.fs[2], s.fs[3]);
+    r.c = make_float4(valid ? s.ray.d[0] : 0.f, valid ? s.ray.d[1] : 0.f,
+                      valid ? s.ray.d[2] : 0.f, valid ? 1.f : 0.f);
+    p.acc[s.out_idx] = r;
+    if (p.stats) {
+        ngprt_ray_stats st;
+        st.marching = s.n_march;
+        st.occupied = s.n_occ;
+        st.occ_acc = s.n_occ_acc;
+        st.dist_acc = s.n_dist;
+        p.stats[s.out_idx] = st;
+    }
+}
+
+// Start the ray of slot `slot` (0..31) of ray tile `tile`. Rays that miss the
+// ROI are written out immediately (black, zero counters) and leave the lane idle.
+__device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, uint32_t slot,
+                                          Lane& s) {
+    const uint32_t cam = tile / p.tiles_per_cam, tt = tile % p.tiles_per_cam;
+    const uint32_t px = (tt % p.tiles_x) * 8 + (slot & 7), py = (tt / p.tiles_x) * 4 + (slot >> 3);
+    s.has_ray = false;
+    if (px >= p.w || py >= p.h) return;
+    s.out_idx = (cam * p.h + py) * p.w + px;
+    s.cd[0] = s.cd[1] = s.cd[2] = 0.f;
+    s.fs[0] = s.fs[1] = s.fs[2] = s.fs[3] = 0.f;
+    s.T = 1.0f;
+    s.n_march = s.n_occ = s.n_occ_acc = s.n_dist = 0;
+    s.pending = false;
+    const bool valid =
+        generate_ray(p.cams[cam], double(p.x0 + px) + 0.5, double(p.y0 + py) + 0.5, s.ray);
+    float t0, t1;
+    if (valid && clip_f(s.ray, t0, t1)) {
+        s.t = t0;
+        s.t1 = t1;
+        s.has_ray = true;
+    } else {
+        write_result(p, s, valid);
+    }
+}
+
+// One marching point (march, occupancy.hpp:310-324): probe (:218-231) via the
+// per-level-1 probe code; occupied -> park for decode; empty -> next_step (:261-276).
+// Returns false when the ray left the clip interval.
+__device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParams& p, Lane& s) {
+    if (!(s.t < s.t1)) return false;
+    float xu[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        xu[a] = s.ray.o[a] + s.ray.d[a] * s.t;  // Ray::at (volume.hpp:19)
+        s.xc[a] = clamp_ref(xu[a], -1.0f, 1.0f);
+    }
+    ++s.n_march;
+    const int r0 = sc.occ_res[0], r1 = sc.occ_res[1];
+    int i0[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) i0[a] = voxel_1d(s.xc[a], sc.occ_h0, r0);
+    // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
+    const uint32_t pidx =
+        uint32_t(i0[0] >> 1) + uint32_t(r1) * (uint32_t(i0[1] >> 1) + uint32_t(r1) * uint32_t(i0[2] >> 1));
+    const uint32_t code = __ldg(sc.probe + pidx);
+    const int e = int(code >> 8) & 7;
+    int exit_k;
+    if (e == 4) {
+        s.n_occ_acc += 5;
+        const uint32_t bi = uint32_t(i0[0]) + uint32_t(r0) * (uint32_t(i0[1]) + uint32_t(r0) * uint32_t(i0[2]));
+        if ((__ldg(sc.occ[0] + (bi >> 5)) >> (bi & 31u)) & 1u) {
+            ++s.n_occ;
+            s.pending = true;
+            return true;
+        }
+        exit_k = 0;
+    } else {
+        s.n_occ_acc += uint32_t(e) + 1u;
+        exit_k = 4 - e;
+    }
+    // voxel_exit_step (occupancy.hpp:238-255) on the unclamped point
+    int iu[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) iu[a] = (xu[a] == s.xc[a]) ? i0[a] : voxel_1d(xu[a], sc.occ_h0, r0);
+    const int res = sc.occ_res[exit_k];
+    float t_exit = 3.402823466e38f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float d = s.ray.d[a];
+        if (d == 0.0f) continue;
+        const float v2 = 2.0f * float(iu[a] >> exit_k);
+        // T(extent)*T(v)/T(res): a power-of-two divisor is an exact reciprocal multiply
+        const float lo = -1.0f + (sc.occ_pow2 ? v2 * sc.lvl_inv_res[exit_k] : v2 / float(res));
+        const float hi = lo + sc.lvl_two_over_res[exit_k];
+        const float bound = d > 0.0f ? hi : lo;
+        const float tc = (bound - s.ray.o[a]) / d;
+        t_exit = (tc < t_exit) ? tc : t_exit;
+    }
+    float sz = t_exit - s.t;
+    if (!(sz > 0.0f)) sz = 0.0f;
+    const float s_occ = sz + 1e-6f;
+    float step = s_occ;
+    if (p.use_grid && sc.dist && res < sc.dist_res) {
+        ++s.n_dist;
+        uint32_t g;
+        if (sc.dist_is_l1) {
+            const int vx = iu[0] >> 1, vy = iu[1] >> 1, vz = iu[2] >> 1;
+            const uint32_t di = uint32_t(vx) + uint32_t(r1) * (uint32_t(vy) + uint32_t(r1) * uint32_t(vz));
+            g = (di == pidx) ? (code & 0xffu) : uint32_t(__ldg(sc.dist + di));
+        } else {
+            const int gr = sc.dist_res;
+            const int vx = voxel_1d(xu[0], sc.dist_h, gr), vy = voxel_1d(xu[1], sc.dist_h, gr),
+                      vz = voxel_1d(xu[2], sc.dist_h, gr);
+            g = __ldg(sc.dist + (size_t(vx) + size_t(gr) * (size_t(vy) + size_t(gr) * vz)));
+        }
+        if (g > 0) {
+            const float s_dist = sc.dist_vox * float(g);
+            step = p.max_step_rule ? ((s_dist < s_occ) ? s_occ : s_dist) : s_dist;
+        }
+    }
+    s.t += step;
+    return true;
+}
+
 template <int L, bool F16>
-__global__ void __launch_bounds__(kBlock) march_kernel(const DevScene sc, const MarchParams p) {
+__global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScene sc,
+                                                                   const MarchParams p) {
     __shared__ unsigned long long tab[32];
     load_exp_table(tab);
     __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const uint32_t total_tiles = p.tiles_per_cam * uint32_t(p.n_cams);
+    const float step = p.step;
 
-    const int cam_i = blockIdx.z;
-    const uint32_t px = blockIdx.x * kTileW + (threadIdx.x % kTileW);
-    const uint32_t py = blockIdx.y * kTileH + (threadIdx.x / kTileW);
-    if (px >= p.w || py >= p.h) return;
-    const CamParams& cam = p.cams[cam_i];
-    const size_t out_idx = (size_t(cam_i) * p.h + py) * p.w + px;
+    uint32_t tile = 0, tile_next_slot = 32;  // warp-uniform tile cursor
+    bool fetch_done = false;                 // warp-uniform
+    Lane s;
+    s.has_ray = false;
+    s.pending = false;
 
-    uint32_t n_march = 0, n_occ = 0, n_occ_acc = 0, n_dist_acc = 0;
-    float cd[3] = {0.f, 0.f, 0.f}, fs[4] = {0.f, 0.f, 0.f, 0.f}, T = 1.0f;
-    Ray ray;
-    const bool valid =
-        generate_ray(cam, double(p.x0 + px) + 0.5, double(p.y0 + py) + 0.5, ray);
-    float t0, t1;
-    if (valid && clip_f(ray, t0, t1)) {
-        const float step = p.step;
-        const bool use_grid = p.use_grid && sc.dist != nullptr;
-        float t = t0;
-        // march, occupancy.hpp:310-324
-        while (t < t1) {
-            float x[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) x[a] = clamp_ref(ray.o[a] + ray.d[a] * t, -1.0f, 1.0f);
-            ++n_march;
-            // occupancy_probe (:218-231): the 5 bit reads are independent, so
-            // issue them together; count only up to the first empty level.
-            bool bits[NGPRT_PYRAMID_LEVELS];
-#pragma unroll
-            for (int k = NGPRT_PYRAMID_LEVELS - 1; k >= 0; --k) {
-                const int res = sc.occ_res[k];
-                bits[k] = occ_bit(sc.occ[k], res, voxel_1d(x[0], res), voxel_1d(x[1], res),
-                                  voxel_1d(x[2], res));
+    while (true) {
+        // ---- refill idle lanes from the warp's tile; fetch tiles as needed ----
+        unsigned need = __ballot_sync(kFull, !s.has_ray);
+        while (need && !fetch_done) {
+            if (tile_next_slot == 32) {
+                uint32_t nt = 0;
+                if (lane == 0) nt = atomicAdd(p.work, 1u);
+                nt = __shfl_sync(kFull, nt, 0);
+                if (nt >= total_tiles) {
+                    fetch_done = true;
+                    break;
+                }
+                tile = nt;
+                tile_next_slot = 0;
             }
-            int exit_res = 0;
-#pragma unroll
-            for (int k = NGPRT_PYRAMID_LEVELS - 1; k >= 0; --k) {
-                if (exit_res) continue;
-                ++n_occ_acc;
-                if (!bits[k]) exit_res = sc.occ_res[k];
-            }
-            if (!exit_res) {
-                ++n_occ;
+            const uint32_t avail = 32u - tile_next_slot;
+            const uint32_t take = min(uint32_t(__popc(need)), avail);
+            const uint32_t rank = __popc(need & lt_mask);
+            if (((need >> lane) & 1u) && rank < take) start_ray(p, tile, tile_next_slot + rank, s);
+            tile_next_slot += take;
+            need = __ballot_sync(kFull, !s.has_ray);
+        }
+        const unsigned active = __ballot_sync(kFull, s.has_ray);
+        if (!active) {
+            if (fetch_done) break;
+            continue;
+        }
+        const unsigned parked = __ballot_sync(kFull, s.has_ray && s.pending);
+        const unsigned stepping = active & ~parked;
+        if (parked && (__popc(parked) >= kDecodeMin || stepping == 0)) {
+            // ---- decode phase: emit(t) of the canonical render_ray ----
+            if (s.has_ray && s.pending) {
                 float f[8];
-                decode_point<L, F16>(sc, x, p.keep_level, tab, f);
+                decode_point<L, F16>(sc, s.xc, p.keep_level, tab, f);
                 // composite, volume.hpp:61-70
                 const float sigma = activate_density(f[0], tab);
                 const float a = alpha_from_sigma(sigma, step, tab);
-                const float w = a * T;
+                const float w = a * s.T;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) cd[c] += w * f[1 + c];
+                for (int c = 0; c < 3; ++c) s.cd[c] += w * f[1 + c];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) fs[c] += w * f[4 + c];
-                T = T * (1.0f - a);
-                if (p.early_stop && T < float(2e-3)) break;  // kEarlyStopTransmittance
-                t += step;
-            } else {
-                // next_step, occupancy.hpp:261-276
-                const float s_occ = voxel_exit_step(ray, t, exit_res);
-                float s = s_occ;
-                if (use_grid && exit_res < sc.dist_res) {
-                    const int gr = sc.dist_res;
-                    const int vx = voxel_1d(ray.o[0] + ray.d[0] * t, gr);
-                    const int vy = voxel_1d(ray.o[1] + ray.d[1] * t, gr);
-                    const int vz = voxel_1d(ray.o[2] + ray.d[2] * t, gr);
-                    ++n_dist_acc;
-                    const uint8_t g = __ldg(sc.dist + (size_t(vx) +
-                                                       size_t(gr) * (size_t(vy) + size_t(gr) * vz)));
-                    if (g > 0) {
-                        const float s_dist = float(2.0 / gr) * float(g);
-                        s = p.max_step_rule ? ((s_dist < s_occ) ? s_occ : s_dist) : s_dist;
-                    }
+                for (int c = 0; c < 4; ++c) s.fs[c] += w * f[4 + c];
+                s.T = s.T * (1.0f - a);
+                s.pending = false;
+                if (p.early_stop && s.T < float(2e-3)) {  // kEarlyStopTransmittance
+                    write_result(p, s, true);
+                    s.has_ray = false;
+                } else {
+                    s.t += step;
                 }
-                t += s;
+            }
+        } else if (s.has_ray && !s.pending) {
+            // ---- step phase: cheap empty-space marching ----
+#pragma unroll 1
+            for (int it = 0; it < kStepBurst; ++it) {
+                if (!march_point(sc, p, s)) {
+                    write_result(p, s, true);
+                    s.has_ray = false;
+                    break;
+                }
+                if (s.pending) break;
             }
         }
-    }
-    RayAcc r;
-    r.a = make_float4(cd[0], cd[1], cd[2], T);
-    r.b = make_float4(fs[0], fs[1], fs[2], fs[3]);
-    r.c = make_float4(valid ? ray.d[0] : 0.f, valid ? ray.d[1] : 0.f, valid ? ray.d[2] : 0.f,
-                      valid ? 1.f : 0.f);
-    p.acc[out_idx] = r;
-    if (p.stats) {
-        ngprt_ray_stats st;
-        st.marching = n_march;
-        st.occupied = n_occ;
-        st.occ_acc = n_occ_acc;
-        st.dist_acc = n_dist_acc;
-        p.stats[out_idx] = st;
     }
 }
 
 template <int L, bool F16>
+int ctas_per_sm_t() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<L, F16>, kBlock, 0);
+    return n > 0 ? n : 1;
+}
+
+template <int L, bool F16>
 void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
-    dim3 grid((p.w + kTileW - 1) / kTileW, (p.h + kTileH - 1) / kTileH, p.n_cams);
-    march_kernel<L, F16><<<grid, kBlock, 0, st>>>(sc, p);
+    static int grid = 0;
+    if (!grid) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = sms * ctas_per_sm_t<L, F16>();
+    }
+    const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);
+    const uint32_t need = (tiles + 3) / 4;  // 4 warps per CTA
+    march_kernel<L, F16><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
+}
+
+// Probe codes (see DevScene::probe).
+__global__ void probe_code_kernel(const DevScene sc, uint16_t* __restrict__ out) {
+    const int r1 = sc.occ_res[1];
+    const size_t n = size_t(r1) * r1 * r1;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int x = int(i % r1), y = int((i / r1) % r1), z = int(i / (size_t(r1) * r1));
+        int e = 0;
+#pragma unroll
+        for (int k = 4; k >= 1; --k) {
+            const int r = sc.occ_res[k], sh = k - 1;
+            const size_t b = size_t(x >> sh) + size_t(r) * (size_t(y >> sh) + size_t(r) * size_t(z >> sh));
+            if (!((sc.occ[k][b >> 5] >> (b & 31)) & 1u)) break;
+            ++e;
+        }
+        const uint32_t g = (sc.dist && sc.dist_is_l1) ? sc.dist[i] : 0u;
+        out[i] = uint16_t((e << 8) | g);
+    }
 }
 
 }  // namespace
@@ -415,6 +587,20 @@ void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
         case 3: f16 ? launch_t<3, true>(sc, p, st) : launch_t<3, false>(sc, p, st); break;
         default: f16 ? launch_t<4, true>(sc, p, st) : launch_t<4, false>(sc, p, st); break;
     }
+}
+
+int march_ctas_per_sm(const DevScene& sc) {
+    const bool f16 = sc.storage == NGPRT_STORAGE_F16;
+    switch (sc.L) {
+        case 1: return f16 ? ctas_per_sm_t<1, true>() : ctas_per_sm_t<1, false>();
+        case 2: return f16 ? ctas_per_sm_t<2, true>() : ctas_per_sm_t<2, false>();
+        case 3: return f16 ? ctas_per_sm_t<3, true>() : ctas_per_sm_t<3, false>();
+        default: return f16 ? ctas_per_sm_t<4, true>() : ctas_per_sm_t<4, false>();
+    }
+}
+
+void launch_probe_codes(const DevScene& sc, uint16_t* out, cudaStream_t st) {
+    probe_code_kernel<<<148 * 8, 256, 0, st>>>(sc, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -109,6 +109,7 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         return fail(NGPRT_EINVAL, "invariant attention mode needs att_globals (baking.hpp:480)");
     if (d->occ_base_res < 16 || d->occ_base_res % 16)
         return fail(NGPRT_EINVAL, "occ_base_res must be a positive multiple of 16");
+    if (d->occ_base_res > 1024) return fail(NGPRT_EUNSUPPORTED, "occ_base_res > 1024");
     if (!d->pyramid_words[0]) return fail(NGPRT_EINVAL, "pyramid level 0 is required");
     if (d->n_coarse && (!d->coarse_keys || !d->coarse_rows))
         return fail(NGPRT_EINVAL, "coarse keys/rows missing");
@@ -149,6 +150,15 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         return fail(NGPRT_ENODEV, std::string("this build targets sm_100a (B200); device is ") +
                                       prop.name);
     NG_CUDA(cudaSetDevice(device));
+    {
+        // Per-render scratch comes from the device's stream-ordered pool; keep its
+        // memory mapped across synchronisations instead of trimming to zero.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~uint64_t(0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
 
     // --- storage decision: fp16 only when lossless ---
     int storage = d->storage;
@@ -298,6 +308,28 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         ds.dist = nullptr;
         ds.dist_res = 0;
     }
+    // --- derived constants: each is the float the reference computes in place ---
+    {
+        const int r0 = ds.occ_res[0];
+        ds.occ_h0 = float(r0) / 2.0f;                     // to_grid_coord, hash_grid.hpp:23-26
+        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) {
+            ds.lvl_two_over_res[k] = 2.0f / float(ds.occ_res[k]);  // occupancy.hpp:247
+            ds.lvl_inv_res[k] = 1.0f / float(ds.occ_res[k]);
+        }
+        ds.occ_pow2 = (r0 & (r0 - 1)) == 0;
+        ds.dist_is_l1 = ds.dist_res != 0 && ds.dist_res == ds.occ_res[1];
+        ds.dist_h = ds.dist_res ? float(ds.dist_res) / 2.0f : 0.f;
+        ds.dist_vox = ds.dist_res ? float(2.0 / ds.dist_res) : 0.f;  // DistanceGrid::voxel_size
+        ds.coarse_h = float(ds.L_C) / 2.0f;
+        for (int l = 0; l < L; ++l) ds.fine_h[l] = float(ds.fine_res[l]) / 2.0f;
+        ds.coarse_u32 = n_corner < (uint64_t(1) << 32);
+        const size_t r1 = size_t(ds.occ_res[1]);
+        uint16_t* probe;
+        NG_TRY(s->alloc(&probe, r1 * r1 * r1 * 2));
+        ds.probe = probe;
+        launch_probe_codes(ds, probe, st);
+        NG_TRY(cudaGetLastError());
+    }
     // --- psi (packed f32 for the exact path; tcgen05 operand image for the tensor path) ---
     {
         std::vector<float> packed(kPsiTotal);
@@ -378,7 +410,9 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     const size_t per_cam = size_t(W) * H;
     RayAcc* acc = nullptr;
     const int chunk = std::min(n_cams, kMaxCamsPerLaunch);
-    NG_CUDA(cudaMallocAsync(&acc, per_cam * chunk * sizeof(RayAcc), st));
+    const size_t acc_bytes = per_cam * chunk * sizeof(RayAcc);
+    NG_CUDA(cudaMallocAsync(&acc, acc_bytes + 256, st));
+    unsigned int* work = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(acc) + acc_bytes);
     cudaStreamAttrValue saved{};
     set_l2_window(s, st, &saved);
     MarchParams p{};
@@ -392,6 +426,9 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     p.early_stop = o->early_stop;
     p.keep_level = o->keep_level;
     p.acc = acc;
+    p.work = work;
+    p.tiles_x = (W + 7) / 8;
+    p.tiles_per_cam = p.tiles_x * ((H + 3) / 4);
     std::unique_lock<std::mutex> prof_lock(s->prof_mu, std::defer_lock);
     if (o->profile) {
         prof_lock.lock();
@@ -413,6 +450,7 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         }
         p.stats = stats ? stats + size_t(c0) * per_cam : nullptr;
         const int li = s->prof_launches;
+        NG_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned int), st));
         if (o->profile) cudaEventRecord(s->prof_event(3 * li), st);
         launch_march(s->ds, p, st);
         if (o->profile) cudaEventRecord(s->prof_event(3 * li + 1), st);

@@ -19,14 +19,19 @@ struct MarchParams {
     CamParams cams[kMaxCamsPerLaunch];
     int n_cams;
     uint32_t x0, y0, w, h;
+    uint32_t tiles_x, tiles_per_cam;  // 8x4 ray tiles over the window
     float step;
     int use_grid, max_step_rule, early_stop, keep_level;
     RayAcc* acc;              // n_cams x h x w
     ngprt_ray_stats* stats;   // nullable, n_cams x h x w
+    unsigned int* work;       // tile counter (zeroed before launch)
 };
 
-// K1: march + gather + fuse + composite (one thread per ray).
+// K1: march + gather + fuse + composite. Persistent warps, one ray per lane,
+// lanes refilled from a global tile counter.
 void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st);
+int march_ctas_per_sm(const DevScene& sc);
+void launch_probe_codes(const DevScene& sc, uint16_t* out, cudaStream_t st);
 // K2 (exact): f32 CUDA-core deferred MLP in the reference's operation order.
 void launch_shade_exact(const DevScene& sc, const RayAcc* acc, float* rgb, size_t n_rays,
                         cudaStream_t st);
