@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c3_1080p")
-    ap.add_argument("--mlp", choices=["tensor", "exact"], default=os.environ.get("NGPRT_MLP", "exact"))
+    ap.add_argument("--mlp", choices=["tensor", "exact"], default=os.environ.get("NGPRT_MLP", "tensor"))
     ap.add_argument("--no-l2-flush", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target wall time of the bounded CPU baseline sample")

@@ -1,8 +1,334 @@
-// mlp_tc.cu — K2 (tensor mode): placeholder until the tcgen05 kernel lands.
-#include "render.cuh"
+// mlp_tc.cu — K2 (tensor mode): the deferred view MLP psi (23 -> 64 -> 64 -> 3,
+// shade, volume.hpp:118-137) on the 5th-generation tensor cores.
+//
+// Persistent CTAs of 128 threads own 128 TMEM columns (two 128x64 f32
+// accumulators). Per tile of 128 rays (M = 128, one ray per TMEM lane):
+//   1. each thread builds its ray's input row [C_d, F, sh(dir)] (23, zero-padded
+//      to K = 32) and stores it to shared memory as a bf16 hi/lo split in the
+//      UMMA canonical K-major no-swizzle layout;
+//   2. one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (bf16 in,
+//      f32 accumulate in TMEM) for x_hi*W_hi + x_lo*W_hi + x_hi*W_lo — three
+//      bf16 products recover ~17 bits of every operand, so the f32 reference is
+//      matched to ~1e-5 (north_star bar: 1e-3) — and commits to an mbarrier;
+//   3. every thread tcgen05.ld's its own TMEM lane (64 f32), adds the bias,
+//      applies ReLU and writes the hidden row back to shared memory (split
+//      again) for layer 2;
+//   4. layer 3 (64 -> 3) runs on CUDA cores from TMEM, then
+//      rgb = sigmoid(C_d + out) with the glibc-expf sigmoid; rays with
+//      final_t == 1 stay black.
 #include <cstring>
+
+#include "render.cuh"
+
 namespace ngprt_dev {
-size_t psi_tc_bytes() { return 16; }
-void pack_psi_tc(const float*, void* out) { std::memset(out, 0, 16); }
-void launch_shade_tensor(const DevScene&, const void*, const RayAcc*, float*, size_t, cudaStream_t) {}
+namespace {
+
+constexpr int kM = 128;        // rays per tile = TMEM lanes
+constexpr int kK1 = 32;        // layer-1 K (23 inputs zero-padded)
+constexpr int kH = 64;         // hidden width = layer-1/2 N
+constexpr int kThreads = 128;
+
+// Operand image layout (bytes), shared by the host packer and the kernel.
+// Every matrix is bf16, K-major, canonical no-swizzle: 8x16B core matrices,
+// offset(r, k) = (r/8)*SBO + (k/8)*128 + (r%8)*16 + (k%8)*2 with SBO = (K/8)*128.
+constexpr int kW1Bytes = kH * kK1 * 2;                 // 4096
+constexpr int kW2Bytes = kH * kH * 2;                  // 8192
+constexpr int kOffW1h = 0, kOffW1l = kOffW1h + kW1Bytes, kOffW2h = kOffW1l + kW1Bytes,
+              kOffW2l = kOffW2h + kW2Bytes, kOffF32 = kOffW2l + kW2Bytes;  // 24576
+// f32 tail: b0[64], b1[64], W2[3][64], b2[3] (+1 pad)
+constexpr int kF32Count = 64 + 64 + 192 + 4;
+constexpr int kImageBytes = kOffF32 + kF32Count * 4;
+// activations: hi/lo planes of a 128 x 64 tile (layer 1 uses the first K = 32 part)
+constexpr int kActBytes = kM * kH * 2;                 // 16384 per plane
+constexpr int kSmemBytes = kImageBytes + 2 * kActBytes + 64;
+
+__host__ __device__ constexpr uint32_t canon_off(int r, int k, int K) {
+    return uint32_t((r / 8) * ((K / 8) * 128) + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2);
+}
+
+__host__ __device__ inline uint16_t f2bf(float f) {  // round to nearest even
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t((u >> 16) | 0x40);  // nan
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return uint16_t(u >> 16);
+}
+__host__ __device__ inline float bf2f(uint16_t h) {
+    uint32_t u = uint32_t(h) << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+// SMEM matrix descriptor (tcgen05 "shared memory descriptor"): start >> 4,
+// LBO >> 4 at [16,30), SBO >> 4 at [32,46), version 1 at [46,48), no swizzle.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return uint64_t((saddr >> 4) & 0x3fffu) | (uint64_t((lbo >> 4) & 0x3fffu) << 16) |
+           (uint64_t((sbo >> 4) & 0x3fffu) << 32) | (uint64_t(1) << 46);
+}
+
+// Instruction descriptor: f32 accumulate, bf16 A/B, K-major both, N = 64, M = 128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kH >> 3) << 17) |
+                            (uint32_t(kM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, {%5, %5, %5, %5}, p;\n\t}\n"
+        :
+        : "r"(d_tmem), "l"(a), "l"(b), "r"(acc), "r"(kIdesc), "r"(0u));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}\n"
+        :: "r"(mbar), "r"(phase) : "memory");
+}
+
+// 64 consecutive f32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+    uint32_t r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+        "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+        "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]),
+          "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),
+          "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+          "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]),
+          "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]),
+          "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Store one row of K values as bf16 hi/lo into the two canonical planes.
+template <int K>
+__device__ __forceinline__ void store_row_split(uint8_t* hi, uint8_t* lo, int row, const float* x) {
+#pragma unroll
+    for (int c = 0; c < K / 8; ++c) {
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float a = x[8 * c + 2 * j], b = x[8 * c + 2 * j + 1];
+            const uint16_t ah = f2bf(a), bh = f2bf(b);
+            const uint16_t al = f2bf(a - bf2f(ah)), bl = f2bf(b - bf2f(bh));
+            h[j] = uint32_t(ah) | (uint32_t(bh) << 16);
+            l[j] = uint32_t(al) | (uint32_t(bl) << 16);
+        }
+        const uint32_t off = canon_off(row, 8 * c, K);
+        *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+}
+
+// One layer: D[tmem] = A(hi,lo) x B(hi,lo)^T over K, three bf16 products.
+template <int K>
+__device__ __forceinline__ void issue_layer(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
+                                            uint32_t b_hi, uint32_t b_lo) {
+    constexpr uint32_t sbo = (K / 8) * 128, lbo = 128;
+#pragma unroll
+    for (int s = 0; s < K / 16; ++s) {
+        const uint32_t ko = uint32_t(s) * 256;  // two 8-element core columns per K = 16 step
+        const uint64_t ah = smem_desc(a_hi + ko, lbo, sbo), al = smem_desc(a_lo + ko, lbo, sbo);
+        const uint64_t bh = smem_desc(b_hi + ko, lbo, sbo), bl = smem_desc(b_lo + ko, lbo, sbo);
+        mma_bf16(d_tmem, ah, bh, s > 0 ? 1u : 0u);
+        mma_bf16(d_tmem, al, bh, 1u);
+        mma_bf16(d_tmem, ah, bl, 1u);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    shade_tc_kernel(const uint8_t* __restrict__ image, const RayAcc* __restrict__ acc,
+                    float* __restrict__ rgb, size_t n_rays) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* w_img = smem;
+    uint8_t* act_hi = smem + kImageBytes;
+    uint8_t* act_lo = act_hi + kActBytes;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(act_lo + kActBytes);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+    __shared__ unsigned long long tab[32];
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    load_exp_table(tab);
+    for (int i = tid; i < kImageBytes / 16; i += kThreads)
+        reinterpret_cast<uint4*>(w_img)[i] = reinterpret_cast<const uint4*>(image)[i];
+    const uint32_t s_mbar = uint32_t(__cvta_generic_to_shared(mbar));
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(s_mbar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;"
+                     :: "r"(uint32_t(__cvta_generic_to_shared(tmem_slot))));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t d1 = tmem, d2 = tmem + kH;                 // column offsets
+    const uint32_t lane_base = uint32_t(warp * 32) << 16;     // this warp's TMEM lanes
+    const float* f32 = reinterpret_cast<const float*>(w_img + kOffF32);
+    const float* b0 = f32;
+    const float* b1 = f32 + 64;
+    const float* w2 = f32 + 128;
+    const float* b2 = f32 + 320;
+    const uint32_t s_w = uint32_t(__cvta_generic_to_shared(w_img));
+    const uint32_t s_ahi = uint32_t(__cvta_generic_to_shared(act_hi));
+    const uint32_t s_alo = uint32_t(__cvta_generic_to_shared(act_lo));
+    uint32_t phase = 0;
+
+    const size_t n_tiles = (n_rays + kM - 1) / kM;
+    for (size_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const size_t ray = tile * kM + tid;
+        RayAcc r;
+        bool shade = false;
+        if (ray < n_rays) {
+            r = acc[ray];
+            shade = r.c.w != 0.f && r.a.w < 1.0f;
+        }
+        // ---- layer 1 input row: [C_d, F, sh(dir)], zero-padded to K = 32 ----
+        float x[kK1];
+#pragma unroll
+        for (int i = 0; i < kK1; ++i) x[i] = 0.f;
+        if (shade) {
+            x[0] = r.a.x; x[1] = r.a.y; x[2] = r.a.z;
+            x[3] = r.b.x; x[4] = r.b.y; x[5] = r.b.z; x[6] = r.b.w;
+            sh_encode(r.c.x, r.c.y, r.c.z, x + 7);
+        }
+        store_row_split<kK1>(act_hi, act_lo, tid, x);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            issue_layer<kK1>(d1, s_ahi, s_alo, s_w + kOffW1h, s_w + kOffW1l);
+            mma_commit(s_mbar);
+        }
+        mbar_wait(s_mbar, phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // ---- layer 1 epilogue -> layer 2 operand ----
+        float h[kH];
+        tmem_ld64(lane_base | d1, h);
+#pragma unroll
+        for (int i = 0; i < kH; ++i) {
+            const float v = h[i] + b0[i];
+            h[i] = v < 0.f ? 0.f : v;
+        }
+        __syncwarp();
+        store_row_split<kH>(act_hi, act_lo, tid, h);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            issue_layer<kH>(d2, s_ahi, s_alo, s_w + kOffW2h, s_w + kOffW2l);
+            mma_commit(s_mbar);
+        }
+        mbar_wait(s_mbar, phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // ---- layer 2 epilogue + layer 3 (64 -> 3) on CUDA cores ----
+        tmem_ld64(lane_base | d2, h);
+        float y[3] = {b2[0], b2[1], b2[2]};
+#pragma unroll
+        for (int i = 0; i < kH; ++i) {
+            float v = h[i] + b1[i];
+            v = v < 0.f ? 0.f : v;
+            y[0] = fmaf(w2[i], v, y[0]);
+            y[1] = fmaf(w2[64 + i], v, y[1]);
+            y[2] = fmaf(w2[128 + i], v, y[2]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        if (ray < n_rays) {
+            float o[3] = {0.f, 0.f, 0.f};
+            if (shade) {
+                o[0] = activate_sigmoid(r.a.x + y[0], tab);
+                o[1] = activate_sigmoid(r.a.y + y[1], tab);
+                o[2] = activate_sigmoid(r.a.z + y[2], tab);
+            }
+            rgb[3 * ray] = o[0];
+            rgb[3 * ray + 1] = o[1];
+            rgb[3 * ray + 2] = o[2];
+        }
+        __syncthreads();  // activations are rewritten by the next tile
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" :: "r"(tmem));
+    }
+}
+
+}  // namespace
+
+size_t psi_tc_bytes() { return size_t(kImageBytes); }
+
+// Packs psi (kPsi* layout, f32) into the kernel's operand image: W0 (64x23,
+// zero-padded to K = 32) and W1 (64x64) as bf16 hi/lo canonical K-major
+// planes, then b0, b1, W2 (3x64), b2 as f32.
+void pack_psi_tc(const float* psi, void* out_v) {
+    auto* out = static_cast<uint8_t*>(out_v);
+    std::memset(out, 0, kImageBytes);
+    auto put = [&](int off_hi, int off_lo, int n, int K, int kin, const float* W) {
+        for (int r = 0; r < n; ++r)
+            for (int k = 0; k < kin; ++k) {
+                const float v = W[r * kin + k];
+                const uint16_t h = f2bf(v), l = f2bf(v - bf2f(h));
+                const uint32_t o = canon_off(r, k, K);
+                std::memcpy(out + off_hi + o, &h, 2);
+                std::memcpy(out + off_lo + o, &l, 2);
+            }
+    };
+    put(kOffW1h, kOffW1l, kH, kK1, 23, psi + kPsiW0);
+    put(kOffW2h, kOffW2l, kH, kH, kH, psi + kPsiW1);
+    float* f = reinterpret_cast<float*>(out + kOffF32);
+    std::memcpy(f, psi + kPsiB0, 64 * 4);
+    std::memcpy(f + 64, psi + kPsiB1, 64 * 4);
+    std::memcpy(f + 128, psi + kPsiW2, 192 * 4);
+    std::memcpy(f + 320, psi + kPsiB2, 3 * 4);
+}
+
+void launch_shade_tensor(const DevScene&, const void* psi_tc, const RayAcc* acc, float* rgb,
+                         size_t n_rays, cudaStream_t st) {
+    if (!n_rays) return;
+    static int grid = 0;
+    if (!grid) {
+        cudaFuncSetAttribute(shade_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shade_tc_kernel, kThreads,
+                                                      kSmemBytes);
+        per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);  // 4 x 128 TMEM columns = 512
+        grid = sms * per_sm;
+    }
+    const size_t tiles = (n_rays + kM - 1) / kM;
+    const int blocks = int(tiles < size_t(grid) ? tiles : size_t(grid));
+    shade_tc_kernel<<<blocks, kThreads, kSmemBytes, st>>>(
+        static_cast<const uint8_t*>(psi_tc), acc, rgb, n_rays);
+}
+
 }  // namespace ngprt_dev

@@ -393,8 +393,6 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         return fail(NGPRT_EINVAL, "level_masked_fine: keep_level out of range (fusion.hpp:201-202)");
     if (o->mlp_mode != NGPRT_MLP_EXACT && o->mlp_mode != NGPRT_MLP_TENSOR)
         return fail(NGPRT_EINVAL, "unknown mlp_mode");
-    if (o->mlp_mode == NGPRT_MLP_TENSOR)
-        return fail(NGPRT_EUNSUPPORTED, "tensor-core MLP not built yet");
     const bool window = o->w && o->h;
     const uint32_t W = window ? o->w : cams[0].width, H = window ? o->h : cams[0].height;
     for (int c = 0; c < n_cams; ++c) {

@@ -150,7 +150,7 @@ class Opts:
     max_step_rule: bool = False
     early_stop: bool = True
     keep_level: int = 0
-    mlp: str = "exact"           # "exact" (bit-exact CUDA cores) | "tensor" (tcgen05)
+    mlp: str = "tensor"          # "tensor" (tcgen05, <= 1e-3) | "exact" (bit-exact CUDA cores)
     window: tuple | None = None  # (x0, y0, w, h)
     profile: bool = False        # per-kernel CUDA-event timing (render_timing())
 
