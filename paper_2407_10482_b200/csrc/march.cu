@@ -205,11 +205,59 @@ __device__ __forceinline__ void corner_weights(const float f[3], float w[8]) {
     for (int k = 0; k < 8; ++k) w[k] = wxy[k & 3] * wz[k >> 2];
 }
 
+// Interpolate fine level l at x (hash_grid.hpp:97-106: out[c] = sum_k w_k row_k[c],
+// corner order k = 0..7 from a zero start). Power-of-two hashed tables take the
+// unrolled path; direct / generic-length levels a compact loop (rare).
+template <bool F16>
+__device__ __forceinline__ void fine_level(const DevScene& sc, int l, const float x[3],
+                                           float fine[8]) {
+    int b[3];
+    float f[3];
+    const float h = sc.fine_h[l];
+    const int res = sc.fine_res[l];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) stencil_axis(x[a], h, res, b[a], f[a]);
+    const void* table = sc.fine[l];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) fine[c] = 0.0f;
+    if (sc.fine_mode[l] == 1) {
+        float w[8];
+        corner_weights(f, w);
+        const uint32_t mask = sc.fine_mask[l];
+        const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
+        const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
+        float frow[8][8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            load_fine_row<F16>(table, (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask,
+                               frow[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) fine[c] += w[k] * frow[k][c];
+    } else {
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+            const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+            const float wk = ((dx ? f[0] : 1.0f - f[0]) * (dy ? f[1] : 1.0f - f[1])) *
+                             (dz ? f[2] : 1.0f - f[2]);
+            float row[8];
+            load_fine_row<F16>(table, fine_index(sc, l, b[0] + dx, b[1] + dy, b[2] + dz), row);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) fine[c] += wk * row[c];
+        }
+    }
+}
+
 // decode_point_baked (baking.hpp:68-91) + split_decoder_output (model.hpp:13-22)
 // + level_masked_fine (fusion.hpp:198-209) + fuse (fusion.hpp:107-173).
+// The weighted fuse adds level l's contribution right after that level is
+// interpolated; levels are visited in order, so every sum is formed in the
+// reference's order. `scr` is this thread's 8-float shared-memory scratch.
 template <int L, bool F16>
 __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3], int keep_level,
-                                             const unsigned long long* tab, float out[8]) {
+                                             const unsigned long long* tab, float* scr,
+                                             float out[8]) {
     constexpr int W = 8 + 2 * L;
     // coarse: stencil at L_C, 8 corner rows, interpolation in corner order
     // k = 0..7 from a zero start (baking.hpp:72-78; absent corners are zero rows)
@@ -239,7 +287,7 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
                 for (int i = 0; i < W; ++i) dec[i] += w[k] * rows[k][i];
         } else {
             const unsigned long long R1 = r1;
-#pragma unroll
+#pragma unroll 1
             for (int k = 0; k < 8; ++k) {
                 const unsigned long long key =
                     (unsigned long long)(cb[0] + (k & 1)) +
@@ -247,76 +295,49 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
                           R1 * (unsigned long long)(cb[2] + (k >> 2)));
                 float row[W];
                 load_coarse_row<W, F16>(sc.coarse, key, row);
+                const float wk = (((k & 1) ? cf[0] : 1.0f - cf[0]) *
+                                  (((k >> 1) & 1) ? cf[1] : 1.0f - cf[1])) *
+                                 ((k >> 2) ? cf[2] : 1.0f - cf[2]);
 #pragma unroll
-                for (int i = 0; i < W; ++i) dec[i] += w[k] * row[i];
+                for (int i = 0; i < W; ++i) dec[i] += wk * row[i];
             }
         }
     }
-    // fine levels: stencil, hash, 8 rows, interpolation (hash_grid.hpp:97-106)
-    float fine[L][8];
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-        int b[3];
-        float f[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[l], sc.fine_res[l], b[a], f[a]);
-        float w[8];
-        corner_weights(f, w);
-        unsigned long long idx[8];
-        if (sc.fine_mode[l] == 1) {
-            const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
-            const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                idx[k] = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & sc.fine_mask[l];
-        } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                idx[k] = fine_index(sc, l, b[0] + (k & 1), b[1] + ((k >> 1) & 1), b[2] + (k >> 2));
-        }
-        float frow[8][8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) load_fine_row<F16>(sc.fine[l], idx[k], frow[k]);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) fine[l][c] = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) fine[l][c] += w[k] * frow[k][c];
-    }
-    if (keep_level > 0) {
-#pragma unroll
-        for (int l = 0; l < L; ++l)
-            if (l + 1 != keep_level)
-#pragma unroll
-                for (int c = 1; c < 8; ++c) fine[l][c] = 0.0f;
-    }
-    // effective weights (fusion.hpp:107-137) and the weighted fuse (:143-154)
-    float wo[L], wb[L];
+    // post-sigmoid attention (split_decoder_output, model.hpp:18-21) for the
+    // spatially variant modes: one sigmoid loop over the 2L logits in scratch
     const int mode = sc.fusion;
+    const bool variant = mode == NGPRT_FUSION_SEPARATE_ATT_V || mode == NGPRT_FUSION_SHARED_ATT_V;
+    if (variant) {
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-        if (mode == NGPRT_FUSION_SEPARATE_ATT_V) {
-            wo[l] = activate_sigmoid(dec[8 + 2 * l], tab);
-            wb[l] = activate_sigmoid(dec[9 + 2 * l], tab);
-        } else if (mode == NGPRT_FUSION_SHARED_ATT_V) {
-            wo[l] = wb[l] = activate_sigmoid(dec[8 + 2 * l], tab);
-        } else if (mode == NGPRT_FUSION_SUM) {
-            wo[l] = wb[l] = 1.0f;
-        } else if (mode == NGPRT_FUSION_SHARED_ATT_INV) {
-            wo[l] = wb[l] = sc.att_w[2 * l];
-        } else {
-            wo[l] = sc.att_w[2 * l];
-            wb[l] = sc.att_w[2 * l + 1];
-        }
+        for (int j = 0; j < 2 * L; ++j) scr[j] = dec[8 + j];
+        const int jstep = mode == NGPRT_FUSION_SHARED_ATT_V ? 2 : 1;
+#pragma unroll 1
+        for (int j = 0; j < 2 * L; j += jstep) scr[j] = activate_sigmoid(scr[j], tab);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) out[i] = dec[i];
-#pragma unroll
+    // fine levels, fused in order (fusion.hpp:143-154, effective_weights :107-137)
+#pragma unroll 1
     for (int l = 0; l < L; ++l) {
-        out[0] += wo[l] * fine[l][0];
+        float fine[8];
+        fine_level<F16>(sc, l, x, fine);
+        if (keep_level > 0 && l + 1 != keep_level) {
 #pragma unroll
-        for (int c = 1; c < 8; ++c) out[c] += wb[l] * fine[l][c];
+            for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
+        }
+        float wo, wb;
+        if (variant) {
+            wo = scr[2 * l];
+            wb = mode == NGPRT_FUSION_SEPARATE_ATT_V ? scr[2 * l + 1] : wo;
+        } else if (mode == NGPRT_FUSION_SUM) {
+            wo = wb = 1.0f;
+        } else {
+            wo = sc.att_w[2 * l];
+            wb = mode == NGPRT_FUSION_SHARED_ATT_INV ? wo : sc.att_w[2 * l + 1];
+        }
+        out[0] += wo * fine[0];
+#pragma unroll
+        for (int c = 1; c < 8; ++c) out[c] += wb * fine[c];
     }
 }
 
@@ -348,8 +369,8 @@ __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s
     }
 }
 
-// Start the ray of slot `slot` (0..31) of ray tile `tile`. Rays that miss the
-// ROI are written out immediately (black, zero counters) and leave the lane idle.
+// Start the ray of slot `slot` (0..31) of ray tile `tile` from the K0 ray
+// buffer. Rays K0 already finished (missed the ROI) leave the lane idle.
 __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, uint32_t slot,
                                           Lane& s) {
     const uint32_t cam = tile / p.tiles_per_cam, tt = tile % p.tiles_per_cam;
@@ -357,21 +378,19 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
     s.has_ray = false;
     if (px >= p.w || py >= p.h) return;
     s.out_idx = (cam * p.h + py) * p.w + px;
+    const float4 a = __ldg(p.rays + 2 * size_t(s.out_idx));
+    const float4 b = __ldg(p.rays + 2 * size_t(s.out_idx) + 1);
+    if (!(b.w >= 0.0f)) return;  // K0 wrote the result (generate_rays/clip_to_roi miss)
+    s.ray.o[0] = a.x; s.ray.o[1] = a.y; s.ray.o[2] = a.z;
+    s.ray.d[0] = b.x; s.ray.d[1] = b.y; s.ray.d[2] = b.z;
+    s.t = a.w;
+    s.t1 = b.w;
     s.cd[0] = s.cd[1] = s.cd[2] = 0.f;
     s.fs[0] = s.fs[1] = s.fs[2] = s.fs[3] = 0.f;
     s.T = 1.0f;
     s.n_march = s.n_occ = s.n_occ_acc = s.n_dist = 0;
     s.pending = false;
-    const bool valid =
-        generate_ray(p.cams[cam], double(p.x0 + px) + 0.5, double(p.y0 + py) + 0.5, s.ray);
-    float t0, t1;
-    if (valid && clip_f(s.ray, t0, t1)) {
-        s.t = t0;
-        s.t1 = t1;
-        s.has_ray = true;
-    } else {
-        write_result(p, s, valid);
-    }
+    s.has_ray = true;
 }
 
 // One marching point (march, occupancy.hpp:310-324): probe (:218-231) via the
@@ -457,8 +476,10 @@ template <int L, bool F16>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScene sc,
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
+    __shared__ float scratch[kBlock * 8];
     load_exp_table(tab);
     __syncthreads();
+    float* scr = scratch + threadIdx.x * 8;
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned lt_mask = (1u << lane) - 1u;
     const uint32_t total_tiles = p.tiles_per_cam * uint32_t(p.n_cams);
@@ -503,7 +524,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             // ---- decode phase: emit(t) of the canonical render_ray ----
             if (s.has_ray && s.pending) {
                 float f[8];
-                decode_point<L, F16>(sc, s.xc, p.keep_level, tab, f);
+                decode_point<L, F16>(sc, s.xc, p.keep_level, tab, scr, f);
                 // composite, volume.hpp:61-70
                 const float sigma = activate_density(f[0], tab);
                 const float a = alpha_from_sigma(sigma, step, tab);
@@ -536,6 +557,34 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
     }
 }
 
+// K0: ray generation for every pixel of the window (generate_rays, scene.hpp:211-228,
+// then clip_to_roi<float>, occupancy.hpp:308). Rays that miss are finished here
+// (black, zero counters); the others are queued for K1 as (o, t0), (d, t1).
+__global__ void __launch_bounds__(256) raygen_kernel(const MarchParams p) {
+    const uint32_t px = blockIdx.x * 32 + (threadIdx.x & 31), py = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int cam = blockIdx.z;
+    if (px >= p.w || py >= p.h) return;
+    const uint32_t idx = (uint32_t(cam) * p.h + py) * p.w + px;
+    Ray r;
+    const bool valid = generate_ray(p.cams[cam], double(p.x0 + px) + 0.5, double(p.y0 + py) + 0.5, r);
+    float t0 = 0.f, t1 = -1.0f;
+    const bool march = valid && clip_f(r, t0, t1);
+    float4* out = const_cast<float4*>(p.rays) + 2 * size_t(idx);
+    if (march) {
+        out[0] = make_float4(r.o[0], r.o[1], r.o[2], t0);
+        out[1] = make_float4(r.d[0], r.d[1], r.d[2], t1);
+        return;
+    }
+    out[1] = make_float4(0.f, 0.f, 0.f, -1.0f);
+    RayAcc a;
+    a.a = make_float4(0.f, 0.f, 0.f, 1.0f);
+    a.b = make_float4(0.f, 0.f, 0.f, 0.f);
+    a.c = make_float4(valid ? r.d[0] : 0.f, valid ? r.d[1] : 0.f, valid ? r.d[2] : 0.f,
+                      valid ? 1.f : 0.f);
+    p.acc[idx] = a;
+    if (p.stats) p.stats[idx] = ngprt_ray_stats{0u, 0u, 0u, 0u};
+}
+
 template <int L, bool F16>
 int ctas_per_sm_t() {
     int n = 0;
@@ -552,6 +601,7 @@ void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid = sms * ctas_per_sm_t<L, F16>();
     }
+    raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
     const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);
     const uint32_t need = (tiles + 3) / 4;  // 4 warps per CTA
     march_kernel<L, F16><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);

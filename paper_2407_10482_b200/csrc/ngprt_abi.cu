@@ -370,15 +370,26 @@ ngprt_status ngprt_scene_info_get(const ngprt_scene* s, ngprt_scene_info* info) 
 
 namespace {
 
+// Keep the fine hash tables (random 16 B gathers, the L2-hot working set)
+// resident: an access-policy window over the contiguous fine block, backed by
+// a persisting L2 set-aside sized to it (north_star: "L2-resident through an
+// access-policy window").
 void set_l2_window(const ngprt_scene* s, cudaStream_t st, cudaStreamAttrValue* saved) {
     cudaStreamGetAttribute(st, cudaStreamAttributeAccessPolicyWindow, saved);
-    int max_win = 0;
+    int max_win = 0, max_persist = 0;
     cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
-    if (max_win <= 0 || !s->fine_block) return;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
+    if (max_win <= 0 || max_persist <= 0 || !s->fine_block) return;
+    const size_t win = std::min<size_t>(s->fine_block_bytes, size_t(max_win));
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    const size_t want = std::min<size_t>(win, size_t(max_persist));
+    if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
     cudaStreamAttrValue v{};
     v.accessPolicyWindow.base_ptr = s->fine_block;
-    v.accessPolicyWindow.num_bytes = std::min<size_t>(s->fine_block_bytes, size_t(max_win));
-    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = std::min(1.0f, float(double(cur) / double(win)));
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
@@ -409,8 +420,11 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     RayAcc* acc = nullptr;
     const int chunk = std::min(n_cams, kMaxCamsPerLaunch);
     const size_t acc_bytes = per_cam * chunk * sizeof(RayAcc);
-    NG_CUDA(cudaMallocAsync(&acc, acc_bytes + 256, st));
-    unsigned int* work = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(acc) + acc_bytes);
+    const size_t ray_bytes = per_cam * chunk * 2 * sizeof(float4);
+    NG_CUDA(cudaMallocAsync(&acc, acc_bytes + ray_bytes + 256, st));
+    const float4* rays = reinterpret_cast<const float4*>(reinterpret_cast<char*>(acc) + acc_bytes);
+    unsigned int* work =
+        reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(acc) + acc_bytes + ray_bytes);
     cudaStreamAttrValue saved{};
     set_l2_window(s, st, &saved);
     MarchParams p{};
@@ -425,6 +439,7 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     p.keep_level = o->keep_level;
     p.acc = acc;
     p.work = work;
+    p.rays = rays;
     p.tiles_x = (W + 7) / 8;
     p.tiles_per_cam = p.tiles_x * ((H + 3) / 4);
     std::unique_lock<std::mutex> prof_lock(s->prof_mu, std::defer_lock);

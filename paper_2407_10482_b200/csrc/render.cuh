@@ -25,6 +25,7 @@ struct MarchParams {
     RayAcc* acc;              // n_cams x h x w
     ngprt_ray_stats* stats;   // nullable, n_cams x h x w
     unsigned int* work;       // tile counter (zeroed before launch)
+    const float4* rays;       // K0 -> K1: (o, t0), (d, t1) per ray; t1 < 0 = already finished
 };
 
 // K1: march + gather + fuse + composite. Persistent warps, one ray per lane,
