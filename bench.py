@@ -191,6 +191,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_2407_10482_b200 as ng
+    from paper_2407_10482_b200 import multigpu as mg
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -206,22 +207,21 @@ def run_ours(args):
     opts = ng.Opts(mlp=args.mlp, profile=True)
     stream = torch.cuda.current_stream(dev)
     out = torch.empty((1, H, W, 3), dtype=torch.float32, device=dev)
-    gather = [torch.empty_like(out) for _ in range(world)] if (world > 1 and rank == 0) else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def cam_of(step):
-        return cams[(rank + world * step) % N_CAMS]
+        return cams[mg.camera_of(rank, world, step, N_CAMS)]
 
     def step_fn(step):
         ng.render(scene, [cam_of(step)], opts, out=out, stream=stream)
         if world > 1:
-            dist.gather(out, gather_list=gather, dst=0)
+            mg.gather_frames(out, world)  # NCCL gather of finished frames to rank 0
 
     # per-camera algorithmic bytes from the bit-exact counters (untimed)
     b_store = 2 if info.storage == 2 else 4
     alg = {}
     for s in range(args.warmup + args.steps):
-        c = (rank + world * s) % N_CAMS
+        c = mg.camera_of(rank, world, s, N_CAMS)
         if c not in alg:
             _, st = ng.render(scene, [cams[c]], ng.Opts(mlp=args.mlp), stats=True)
             st = st.cpu().numpy()
@@ -249,7 +249,7 @@ def run_ours(args):
             k1_ms.append(a)
             k2_ms.append(b)
             launches += n
-            bytes_k1 += alg[(rank + world * s) % N_CAMS][0]
+            bytes_k1 += alg[mg.camera_of(rank, world, s, N_CAMS)][0]
     total_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -286,7 +286,7 @@ def run_ours(args):
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
             traffic = json.loads(tp.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
-        mean_stats = np.mean([alg[(rank + world * (args.warmup + i)) % N_CAMS][1]
+        mean_stats = np.mean([alg[mg.camera_of(rank, world, args.warmup + i, N_CAMS)][1]
                               for i in range(args.steps)], axis=0)
         line = {
             "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,

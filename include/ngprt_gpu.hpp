@@ -1,0 +1,124 @@
+// ngprt_gpu.hpp — header-only C++ adapter from the reference's own types to the
+// B200 C ABI (ngprt_cuda.h). This is the binding a maintainer of the reference
+// adds to route its render path to the GPU:
+//
+//     #include "ngprt/baking.hpp"     // reference: BakedScene, PosedDataset, Image
+//     #include "ngprt_gpu.hpp"
+//     ngprt::gpu::Scene gs(baked);                  // upload once (ngprt_scene_create)
+//     ngprt::Image img = gs.render(dataset, frame); // == render_ray over every pixel
+//
+// Requires the reference headers (/root/reference/proj/include) on the include
+// path and links against paper_2407_10482_b200/_lib/libngprt_cuda.so.
+// Errors surface as std::runtime_error carrying ngprt_last_error(), like the
+// reference's own exceptions.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ngprt/baking.hpp"
+#include "ngprt/config.hpp"
+#include "ngprt/scene.hpp"
+#include "ngprt_cuda.h"
+
+namespace ngprt::gpu {
+
+struct RenderOptions {
+    float step = float(kBaseStep);  // march step gamma * s0 (config.hpp:11)
+    bool use_dist_grid = true;      // march(..., &distance, ...) vs nullptr
+    bool max_step_rule = false;     // occupancy.hpp:272
+    bool early_stop = true;         // volume.hpp:70
+    int keep_level = 0;             // level_masked_fine (fusion.hpp:198-209); 0 = off
+    bool exact_mlp = false;         // bit-exact CUDA-core shade instead of tcgen05
+};
+
+inline void check(ngprt_status s, const char* what) {
+    if (s != NGPRT_OK) throw std::runtime_error(std::string(what) + ": " + ngprt_last_error());
+}
+
+// A BakedScene resident on one B200 (immutable).
+class Scene {
+public:
+    explicit Scene(const BakedScene& s, int device = 0) {
+        ngprt_scene_desc d{};
+        const int L = s.cfg.fine_levels;
+        d.L = uint32_t(L);
+        d.L_C = uint32_t(s.cfg.corner_grid_res);
+        // SparseCoarseGrid (baking.hpp:11-50): keys in row order
+        std::vector<uint64_t> keys(s.coarse.index.size());
+        for (const auto& kv : s.coarse.index) keys[kv.second] = kv.first;
+        d.n_coarse = keys.size();
+        d.coarse_keys = keys.data();
+        d.coarse_rows = s.coarse.rows.data();
+        for (int l = 0; l < L; ++l) {
+            d.fine_res[l] = uint32_t(s.fine[l].resolution);
+            d.fine_table_len[l] = s.fine[l].table_len;
+            d.fine_hashed[l] = s.fine[l].addressing == Addressing::Hashed ? 1 : 0;
+            d.fine_tables[l] = s.fine[l].entries.value.data();
+        }
+        for (int k = 0; k < 3; ++k) {
+            d.psi_w[k] = s.psi.weight[k].value.data();
+            d.psi_b[k] = s.psi.bias[k].value.data();
+        }
+        d.fusion_tag = uint8_t(s.tag);
+        d.att_globals = fusion_is_invariant(s.tag) ? s.fusion.global_pre.value.data() : nullptr;
+        d.occ_base_res = uint32_t(s.pyramid.levels[0].res);
+        for (int k = 0; k < kPyramidLevels; ++k) d.pyramid_words[k] = s.pyramid.levels[k].words.data();
+        d.dist_res = uint32_t(s.distance.resolution);
+        d.dist_values = s.distance.values.empty() ? nullptr : s.distance.values.data();
+        check(ngprt_scene_create(&d, device, &h_), "ngprt_scene_create");
+    }
+    ~Scene() { ngprt_scene_destroy(h_); }
+    Scene(const Scene&) = delete;
+    Scene& operator=(const Scene&) = delete;
+
+    // Renders frame `frame` of `ds` (scene.hpp:191-228 camera model) into an Image
+    // (image.hpp:12-22); optionally returns the per-ray MarchCounters.
+    Image render(const PosedDataset& ds, size_t frame, const RenderOptions& o = {},
+                 std::vector<MarchCounters>* counters = nullptr) const {
+        if (frame >= ds.frames.size()) throw std::out_of_range("render: bad frame index");
+        ngprt_camera cam{};
+        for (int i = 0; i < 16; ++i) cam.c2w[i] = ds.frames[frame].c2w[i];
+        cam.fx = ds.fx;
+        cam.fy = ds.fy;
+        cam.cx = ds.cx;
+        cam.cy = ds.cy;
+        cam.width = uint32_t(ds.width);
+        cam.height = uint32_t(ds.height);
+        ngprt_render_opts ro{};
+        ro.step = o.step;
+        ro.use_dist_grid = o.use_dist_grid;
+        ro.max_step_rule = o.max_step_rule;
+        ro.early_stop = o.early_stop;
+        ro.keep_level = int8_t(o.keep_level);
+        ro.mlp_mode = o.exact_mlp ? NGPRT_MLP_EXACT : NGPRT_MLP_TENSOR;
+        Image img(ds.width, ds.height);
+        std::vector<ngprt_ray_stats> st(counters ? size_t(ds.width) * ds.height : 0);
+        check(ngprt_render_host(h_, &cam, 1, &ro, img.rgb.data(), counters ? st.data() : nullptr),
+              "ngprt_render_host");
+        if (counters) {
+            counters->resize(st.size());
+            for (size_t i = 0; i < st.size(); ++i) {
+                (*counters)[i].marching_points = st[i].marching;
+                (*counters)[i].occupied_points = st[i].occupied;
+                (*counters)[i].occ_grid_accesses = st[i].occ_acc;
+                (*counters)[i].dist_grid_accesses = st[i].dist_acc;
+            }
+        }
+        return img;
+    }
+
+    ngprt_scene* handle() const { return h_; }
+
+private:
+    ngprt_scene* h_ = nullptr;
+};
+
+// One-shot convenience: upload, render one frame.
+inline Image render(const BakedScene& s, const PosedDataset& ds, size_t frame,
+                    const RenderOptions& o = {}, int device = 0) {
+    return Scene(s, device).render(ds, frame, o);
+}
+
+}  // namespace ngprt::gpu

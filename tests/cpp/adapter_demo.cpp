@@ -1,0 +1,123 @@
+// tests/cpp/adapter_demo.cpp — drop-in demonstration (test infrastructure).
+//
+// Builds a BakedScene entirely with the reference's own functions (make_scene,
+// scene_occupancy, build_pyramid, build_distance_grid, HashLevel, TinyMlp,
+// FusionMode), renders it (a) with the reference's render path composed on the
+// CPU exactly as SURVEY.md §8(c) and (b) on the B200 through include/ngprt_gpu.hpp,
+// and compares with the reference's own max_abs_diff / psnr (image.hpp:89-110).
+// Feature values are NOT fp16-representable, so the GPU picks f32 storage.
+// Prints one JSON line; tests/test_gpu_adapter.py checks it.
+#include "ngprt_gpu.hpp"
+
+#include <cstdio>
+
+using namespace ngprt;
+
+static BakedScene make_baked(uint64_t seed) {
+    BakedScene s;
+    s.cfg.corner_grid_res = 64;
+    s.cfg.fine_levels = 2;
+    s.cfg.fine_table_len = size_t(1) << 14;
+    s.tag = FusionTag::SeparateAttV;
+    Rng rng(seed);
+    const SynthScene sc = make_scene("toy");
+    s.pyramid = build_pyramid(scene_occupancy(sc, 128));
+    s.distance = build_distance_grid(s.pyramid.levels[1]);
+    const int lc = s.cfg.corner_grid_res, L = s.cfg.fine_levels;
+    s.coarse.init(lc, L);
+    BitGrid occ = scene_occupancy(sc, lc), marks(lc + 1);
+    for (int z = 0; z < lc; ++z)
+        for (int y = 0; y < lc; ++y)
+            for (int x = 0; x < lc; ++x)
+                if (occ.get(x, y, z))
+                    for (int k = 0; k < 8; ++k) marks.set(x + (k & 1), y + ((k >> 1) & 1), z + (k >> 2));
+    for (int z = 0; z <= lc; ++z)
+        for (int y = 0; y <= lc; ++y)
+            for (int x = 0; x <= lc; ++x) {
+                if (!marks.get(x, y, z)) continue;
+                float* row = s.coarse.add_row(s.coarse.key_of({x, y, z}));
+                row[0] = float(rng.uniform(1.0, 5.0));
+                for (int c = 1; c < 8 + 2 * L; ++c) row[c] = float(rng.uniform(-1.5, 1.5));
+            }
+    s.fine.resize(L);
+    for (int l = 0; l < L; ++l) {
+        s.fine[l].init("fine_l" + std::to_string(l + 1), s.cfg.fine_resolution(l),
+                       s.cfg.fine_table_len, kFineFeatureDim);
+        for (auto& v : s.fine[l].entries.value) v = float(rng.uniform(-1.0, 1.0));
+    }
+    s.psi.init({kShadeInWidth, 64, 64, 3}, "psi", rng, nullptr);
+    for (int k = 0; k < 3; ++k)
+        for (auto& b : s.psi.bias[k].value) b = float(rng.uniform(-0.1, 0.1));
+    s.fusion.init(s.tag, L, rng, nullptr);
+    return s;
+}
+
+// The canonical render_ray composition with reference functions.
+static Image cpu_render(const BakedScene& s, const PosedDataset& ds, size_t f,
+                        std::vector<MarchCounters>& mcs) {
+    Image img(ds.width, ds.height);
+    mcs.assign(size_t(ds.width) * ds.height, MarchCounters{});
+    const float step = float(kBaseStep);
+    for (int py = 0; py < ds.height; ++py)
+        for (int px = 0; px < ds.width; ++px) {
+            Ray<float> ray;
+            if (!generate_rays(ds, f, px + 0.5, py + 0.5, ray)) continue;
+            std::vector<RaySample<float>> samples;
+            float T = 1.f;
+            auto emit = [&](float t) {
+                Vec3f x = ray.at(t);
+                for (int a = 0; a < 3; ++a) x[a] = ngprt::clamp(x[a], -1.f, 1.f);
+                auto feat = decode_point_baked(s, x);
+                samples.push_back({t, step, feat});
+                T = T * (1.f - alpha_from_sigma(activate_density(feat.sigma_pre()), step));
+                return !(T < float(kEarlyStopTransmittance));
+            };
+            mcs[size_t(py) * ds.width + px] = march(ray, s.pyramid, &s.distance, step, false, emit);
+            auto acc = composite(std::span<const RaySample<float>>(samples), true);
+            if (acc.final_t < 1.f) {
+                Vec3f c = shade(acc, ray.dir, s.psi);
+                float* p = img.pixel(px, py);
+                p[0] = c[0];
+                p[1] = c[1];
+                p[2] = c[2];
+            }
+        }
+    return img;
+}
+
+int main() {
+    const BakedScene s = make_baked(2024);
+    PosedDataset ds;
+    ds.width = 64;
+    ds.height = 48;
+    ds.fx = ds.fy = 1.1 * ds.width;
+    ds.cx = 0.5 * ds.width;
+    ds.cy = 0.5 * ds.height;
+    for (auto& m : sphere_views(3, 2.9)) ds.frames.push_back({"", m});
+    gpu::Scene gs(s);
+    double worst_exact = 0, worst_tc = 0, min_psnr_tc = 99;
+    long counter_mismatch = 0;
+    for (size_t f = 0; f < ds.frames.size(); ++f) {
+        std::vector<MarchCounters> ref_mc, gpu_mc;
+        const Image ref = cpu_render(s, ds, f, ref_mc);
+        gpu::RenderOptions exact;
+        exact.exact_mlp = true;
+        const Image g_exact = gs.render(ds, f, exact, &gpu_mc);
+        const Image g_tc = gs.render(ds, f);
+        worst_exact = std::max(worst_exact, max_abs_diff(ref, g_exact));
+        worst_tc = std::max(worst_tc, max_abs_diff(ref, g_tc));
+        min_psnr_tc = std::min(min_psnr_tc, psnr(ref, g_tc));
+        for (size_t i = 0; i < ref_mc.size(); ++i)
+            counter_mismatch += ref_mc[i].marching_points != gpu_mc[i].marching_points ||
+                                ref_mc[i].occupied_points != gpu_mc[i].occupied_points ||
+                                ref_mc[i].occ_grid_accesses != gpu_mc[i].occ_grid_accesses ||
+                                ref_mc[i].dist_grid_accesses != gpu_mc[i].dist_grid_accesses;
+    }
+    ngprt_scene_info info{};
+    ngprt_scene_info_get(gs.handle(), &info);
+    std::printf("{\"frames\": %zu, \"max_abs_exact\": %.9g, \"max_abs_tensor\": %.9g, "
+                "\"psnr_tensor\": %.3f, \"counter_mismatch\": %ld, \"storage\": %d}\n",
+                ds.frames.size(), worst_exact, worst_tc, min_psnr_tc, counter_mismatch,
+                int(info.storage));
+    return 0;
+}
