@@ -6,7 +6,7 @@
 // tiles from a global counter; a lane whose ray finishes is refilled from the
 // warp's current tile. Lanes march independently, but a lane that reaches an
 // occupied point parks there until enough lanes of the warp are parked
-// (kDecodeMin) or no lane can step: the expensive sample decode then runs
+// (MarchParams::decode_min) or no lane can step: the expensive sample decode then runs
 // with most lanes converged instead of serialising against cheap empty steps.
 //
 // Parity: built with -fmad=false and every float/double operation is the
@@ -22,8 +22,8 @@ namespace ngprt_dev {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kDecodeMin = 12;  // parked lanes that trigger a warp-wide decode
-constexpr int kStepBurst = 4;   // marching points a stepping lane takes per round
+// MarchParams::decode_min: parked lanes that trigger a warp-wide decode (default 12)
+// MarchParams::step_burst: marching points a stepping lane takes per round (default 4)
 constexpr int kMinBlocks = 5;   // register budget: 65536 / (128 * 5) = 102 regs
 
 struct Ray {
@@ -95,14 +95,14 @@ __device__ __forceinline__ bool clip_f(const Ray& r, float& t0, float& t1) {
 // voxel_of along one axis (occupancy.hpp:94-102) with h = float(res)/2.0f,
 // i.e. to_grid_coord (hash_grid.hpp:23-26) then floor and clamp.
 __device__ __forceinline__ int voxel_1d(float x, float h, int res) {
-    const int i = int(floorf((x - (-1.0f)) * h));
+    const int i = __float2int_rd((x - (-1.0f)) * h);  // == int(floor(u)) for finite u
     return i < 0 ? 0 : (i > res - 1 ? res - 1 : i);
 }
 
 // Stencil along one axis: base index and fractional offset (hash_grid.hpp:38-46).
 __device__ __forceinline__ void stencil_axis(float x, float h, int res, int& base, float& frac) {
     const float u = (x - (-1.0f)) * h;
-    int i = int(floorf(u));
+    int i = __float2int_rd(u);
     i = i < res - 1 ? i : res - 1;
     i = i > 0 ? i : 0;
     base = i;
@@ -402,7 +402,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         xu[a] = s.ray.o[a] + s.ray.d[a] * s.t;  // Ray::at (volume.hpp:19)
-        s.xc[a] = clamp_ref(xu[a], -1.0f, 1.0f);
+        s.xc[a] = fminf(fmaxf(xu[a], -1.0f), 1.0f);  // == clamp (common.hpp:94-97) for non-NaN
     }
     ++s.n_march;
     const int r0 = sc.occ_res[0], r1 = sc.occ_res[1];
@@ -428,31 +428,15 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
         s.n_occ_acc += uint32_t(e) + 1u;
         exit_k = 4 - e;
     }
-    // voxel_exit_step (occupancy.hpp:238-255) on the unclamped point
+    // next_step (occupancy.hpp:261-276) on the unclamped point ray.at(t)
     int iu[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) iu[a] = (xu[a] == s.xc[a]) ? i0[a] : voxel_1d(xu[a], sc.occ_h0, r0);
     const int res = sc.occ_res[exit_k];
-    float t_exit = 3.402823466e38f;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const float d = s.ray.d[a];
-        if (d == 0.0f) continue;
-        const float v2 = 2.0f * float(iu[a] >> exit_k);
-        // T(extent)*T(v)/T(res): a power-of-two divisor is an exact reciprocal multiply
-        const float lo = -1.0f + (sc.occ_pow2 ? v2 * sc.lvl_inv_res[exit_k] : v2 / float(res));
-        const float hi = lo + sc.lvl_two_over_res[exit_k];
-        const float bound = d > 0.0f ? hi : lo;
-        const float tc = (bound - s.ray.o[a]) / d;
-        t_exit = (tc < t_exit) ? tc : t_exit;
-    }
-    float sz = t_exit - s.t;
-    if (!(sz > 0.0f)) sz = 0.0f;
-    const float s_occ = sz + 1e-6f;
-    float step = s_occ;
-    if (p.use_grid && sc.dist && res < sc.dist_res) {
+    uint32_t g = 0;
+    const bool consult = p.use_grid && sc.dist && res < sc.dist_res;
+    if (consult) {
         ++s.n_dist;
-        uint32_t g;
         if (sc.dist_is_l1) {
             const int vx = iu[0] >> 1, vy = iu[1] >> 1, vz = iu[2] >> 1;
             const uint32_t di = uint32_t(vx) + uint32_t(r1) * (uint32_t(vy) + uint32_t(r1) * uint32_t(vz));
@@ -463,9 +447,34 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
                       vz = voxel_1d(xu[2], sc.dist_h, gr);
             g = __ldg(sc.dist + (size_t(vx) + size_t(gr) * (size_t(vy) + size_t(gr) * vz)));
         }
-        if (g > 0) {
+    }
+    float step;
+    if (g > 0 && !p.max_step_rule) {
+        // Eq. 9: a positive distance value replaces s_occ, which has no other use
+        // and no side effect, so voxel_exit_step is skipped (same t sequence).
+        step = sc.dist_vox * float(g);
+    } else {
+        // voxel_exit_step (occupancy.hpp:238-255)
+        float t_exit = 3.402823466e38f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float d = s.ray.d[a];
+            if (d == 0.0f) continue;
+            const float v2 = 2.0f * float(iu[a] >> exit_k);
+            // T(extent)*T(v)/T(res): a power-of-two divisor is an exact reciprocal multiply
+            const float lo = -1.0f + (sc.occ_pow2 ? v2 * sc.lvl_inv_res[exit_k] : v2 / float(res));
+            const float hi = lo + sc.lvl_two_over_res[exit_k];
+            const float bound = d > 0.0f ? hi : lo;
+            const float tc = (bound - s.ray.o[a]) / d;
+            t_exit = (tc < t_exit) ? tc : t_exit;
+        }
+        float sz = t_exit - s.t;
+        if (!(sz > 0.0f)) sz = 0.0f;
+        const float s_occ = sz + 1e-6f;
+        step = s_occ;
+        if (g > 0) {  // max_step_rule
             const float s_dist = sc.dist_vox * float(g);
-            step = p.max_step_rule ? ((s_dist < s_occ) ? s_occ : s_dist) : s_dist;
+            step = (s_dist < s_occ) ? s_occ : s_dist;
         }
     }
     s.t += step;
@@ -520,7 +529,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
         }
         const unsigned parked = __ballot_sync(kFull, s.has_ray && s.pending);
         const unsigned stepping = active & ~parked;
-        if (parked && (__popc(parked) >= kDecodeMin || stepping == 0)) {
+        if (parked && (__popc(parked) >= p.decode_min || stepping == 0)) {
             // ---- decode phase: emit(t) of the canonical render_ray ----
             if (s.has_ray && s.pending) {
                 float f[8];
@@ -545,7 +554,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
         } else if (s.has_ray && !s.pending) {
             // ---- step phase: cheap empty-space marching ----
 #pragma unroll 1
-            for (int it = 0; it < kStepBurst; ++it) {
+            for (int it = 0; it < p.step_burst; ++it) {
                 if (!march_point(sc, p, s)) {
                     write_result(p, s, true);
                     s.has_ray = false;

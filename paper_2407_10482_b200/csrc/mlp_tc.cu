@@ -16,6 +16,8 @@
 //   4. layer 3 (64 -> 3) runs on CUDA cores from TMEM, then
 //      rgb = sigmoid(C_d + out) with the glibc-expf sigmoid; rays with
 //      final_t == 1 stay black.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "render.cuh"
@@ -156,7 +158,7 @@ __device__ __forceinline__ void issue_layer(uint32_t d_tmem, uint32_t a_hi, uint
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 3)
     shade_tc_kernel(const uint8_t* __restrict__ image, const RayAcc* __restrict__ acc,
                     float* __restrict__ rgb, size_t n_rays) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -199,14 +201,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
 
     const size_t n_tiles = (n_rays + kM - 1) / kM;
+    // register double buffer: the next tile's RayAcc is loaded while this tile's
+    // MMAs and epilogues run
+    RayAcc r_next{};
+    if (size_t(blockIdx.x) * kM + tid < n_rays) r_next = acc[size_t(blockIdx.x) * kM + tid];
     for (size_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const size_t ray = tile * kM + tid;
-        RayAcc r;
-        bool shade = false;
-        if (ray < n_rays) {
-            r = acc[ray];
-            shade = r.c.w != 0.f && r.a.w < 1.0f;
-        }
+        const RayAcc r = r_next;
+        const bool shade = ray < n_rays && r.c.w != 0.f && r.a.w < 1.0f;
+        const size_t nray = (tile + gridDim.x) * kM + tid;
+        if (nray < n_rays) r_next = acc[nray];
         // ---- layer 1 input row: [C_d, F, sh(dir)], zero-padded to K = 32 ----
         float x[kK1];
 #pragma unroll
@@ -317,13 +321,29 @@ void launch_shade_tensor(const DevScene&, const void* psi_tc, const RayAcc* acc,
     if (!grid) {
         cudaFuncSetAttribute(shade_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSmemBytes);
+        cudaFuncSetAttribute(shade_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             int(cudaSharedmemCarveoutMaxShared));
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shade_tc_kernel, kThreads,
-                                                      kSmemBytes);
-        per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);  // 4 x 128 TMEM columns = 512
+        const cudaError_t occ_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, shade_tc_kernel, kThreads, kSmemBytes);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, shade_tc_kernel);
+        if (std::getenv("NGPRT_VERBOSE"))
+            std::fprintf(stderr, "[ngprt] shade_tc occupancy=%d (%s) regs=%d static_smem=%zu max_dyn=%d\n",
+                         per_sm, cudaGetErrorString(occ_err), fa.numRegs, fa.sharedSizeBytes,
+                         fa.maxDynamicSharedSizeBytes);
+        // 3 x (58.7 KB smem, 128 TMEM columns, 128 x 165 regs) fit one SM; the
+        // occupancy API reports 1 for this kernel, so the grid is sized explicitly
+        // (surplus CTAs would simply run as a later wave). NGPRT_K2_CTAS overrides.
+        const char* ov = std::getenv("NGPRT_K2_CTAS");
+        per_sm = ov ? std::atoi(ov) : 3;
+        per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
         grid = sms * per_sm;
+        if (std::getenv("NGPRT_VERBOSE"))
+            std::fprintf(stderr, "[ngprt] shade_tc: %d CTAs/SM, grid %d, smem %d B\n", per_sm, grid,
+                         kSmemBytes);
     }
     const size_t tiles = (n_rays + kM - 1) / kM;
     const int blocks = int(tiles < size_t(grid) ? tiles : size_t(grid));

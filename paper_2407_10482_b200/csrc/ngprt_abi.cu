@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -440,6 +441,19 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     p.acc = acc;
     p.work = work;
     p.rays = rays;
+    {
+        // K1 scheduling policy; NGPRT_DECODE_MIN / NGPRT_STEP_BURST override for tuning
+        static const int dmin = [] {
+            const char* e = std::getenv("NGPRT_DECODE_MIN");
+            return e ? std::max(1, std::min(32, std::atoi(e))) : 12;
+        }();
+        static const int burst = [] {
+            const char* e = std::getenv("NGPRT_STEP_BURST");
+            return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
+        }();
+        p.decode_min = dmin;
+        p.step_burst = burst;
+    }
     p.tiles_x = (W + 7) / 8;
     p.tiles_per_cam = p.tiles_x * ((H + 3) / 4);
     std::unique_lock<std::mutex> prof_lock(s->prof_mu, std::defer_lock);

@@ -22,6 +22,7 @@ struct MarchParams {
     uint32_t tiles_x, tiles_per_cam;  // 8x4 ray tiles over the window
     float step;
     int use_grid, max_step_rule, early_stop, keep_level;
+    int decode_min, step_burst;  // K1 warp scheduling policy (tunable, see march.cu)
     RayAcc* acc;              // n_cams x h x w
     ngprt_ray_stats* stats;   // nullable, n_cams x h x w
     unsigned int* work;       // tile counter (zeroed before launch)
