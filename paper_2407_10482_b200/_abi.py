@@ -6,7 +6,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libngprt_cuda.so"
+import os  # noqa: E402
+
+LIB_PATH = Path(os.environ.get("NGPRT_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libngprt_cuda.so")
 
 MAX_FINE_LEVELS = 4
 PYRAMID_LEVELS = 5

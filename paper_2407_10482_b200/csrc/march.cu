@@ -24,7 +24,10 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 // MarchParams::decode_min: parked lanes that trigger a warp-wide decode (default 12)
 // MarchParams::step_burst: marching points a stepping lane takes per round (default 4)
-constexpr int kMinBlocks = 5;   // register budget: 65536 / (128 * 5) = 102 regs
+#ifndef NGPRT_K1_MIN_BLOCKS
+#define NGPRT_K1_MIN_BLOCKS 5
+#endif
+constexpr int kMinBlocks = NGPRT_K1_MIN_BLOCKS;  // 5: 65536 / (128 * 5) = 102 regs
 
 struct Ray {
     float o[3], d[3];
@@ -109,38 +112,37 @@ __device__ __forceinline__ void stencil_axis(float x, float h, int res, int& bas
     frac = u - float(i);
 }
 
+// One 32 B fp16 coarse row (one sector) in a single 256-bit load (sm_100
+// ld.global.v8.b32 -> LDG.E.256). NGPRT_COARSE_L2_HINT selects the L2 eviction
+// priority: 0 normal, 1 evict_first, 2 evict_last.
+#ifndef NGPRT_COARSE_L2_HINT
+#define NGPRT_COARSE_L2_HINT 0
+#endif
+__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
+#if NGPRT_COARSE_L2_HINT == 1
+    asm volatile("ld.global.nc.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#elif NGPRT_COARSE_L2_HINT == 2
+    asm volatile("ld.global.nc.L2::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#else
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#endif
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+
 // Row loads: N leading elements of a 16-element row, converted to f32 (exact).
 template <int N, bool F16>
 __device__ __forceinline__ void load_coarse_row(const void* __restrict__ base,
                                                 unsigned long long row, float* out) {
     if constexpr (F16) {
-        const uint4* p = reinterpret_cast<const uint4*>(base) + row * 2;
-        const uint4 a = __ldg(p);
-        const __half2* ha = reinterpret_cast<const __half2*>(&a);
+        uint32_t r[8];
+        ldg256(reinterpret_cast<const uint4*>(base) + row * 2, r);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float2 f = __half22float2(ha[i]);
+        for (int i = 0; i < N / 2; ++i) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&r[i]));
             out[2 * i] = f.x;
             out[2 * i + 1] = f.y;
-        }
-        if constexpr (N > 12) {
-            const uint4 b = __ldg(p + 1);
-            const __half2* hb = reinterpret_cast<const __half2*>(&b);
-#pragma unroll
-            for (int i = 0; i < (N - 8) / 2; ++i) {
-                const float2 f = __half22float2(hb[i]);
-                out[8 + 2 * i] = f.x;
-                out[9 + 2 * i] = f.y;
-            }
-        } else if constexpr (N > 8) {
-            const uint2 b = __ldg(reinterpret_cast<const uint2*>(p + 1));
-            const __half2* hb = reinterpret_cast<const __half2*>(&b);
-#pragma unroll
-            for (int i = 0; i < (N - 8) / 2; ++i) {
-                const float2 f = __half22float2(hb[i]);
-                out[8 + 2 * i] = f.x;
-                out[9 + 2 * i] = f.y;
-            }
         }
     } else {
         const float4* p = reinterpret_cast<const float4*>(base) + row * 4;
@@ -257,8 +259,30 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
 template <int L, bool F16>
 __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3], int keep_level,
                                              const unsigned long long* tab, float* scr,
-                                             float out[8]) {
+                                             int prefetch, float out[8]) {
     constexpr int W = 8 + 2 * L;
+    if (prefetch) {
+        // The fine rows depend only on x: pull them towards L1 now so the
+        // per-level loads below do not add two more dependent L2 round trips.
+#pragma unroll 1
+        for (int l = 0; l < L; ++l) {
+            if (sc.fine_mode[l] != 1) continue;
+            int b[3];
+            float f[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[l], sc.fine_res[l], b[a], f[a]);
+            const uint32_t mask = sc.fine_mask[l];
+            const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
+            const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
+            const char* base = static_cast<const char*>(sc.fine[l]);
+            const int rb = F16 ? 16 : 32;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t idx = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(base + size_t(idx) * rb));
+            }
+        }
+    }
     // coarse: stencil at L_C, 8 corner rows, interpolation in corner order
     // k = 0..7 from a zero start (baking.hpp:72-78; absent corners are zero rows)
     float dec[W];
@@ -533,7 +557,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             // ---- decode phase: emit(t) of the canonical render_ray ----
             if (s.has_ray && s.pending) {
                 float f[8];
-                decode_point<L, F16>(sc, s.xc, p.keep_level, tab, scr, f);
+                decode_point<L, F16>(sc, s.xc, p.keep_level, tab, scr, p.prefetch, f);
                 // composite, volume.hpp:61-70
                 const float sigma = activate_density(f[0], tab);
                 const float a = alpha_from_sigma(sigma, step, tab);

@@ -163,6 +163,9 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
 
     // --- storage decision: fp16 only when lossless ---
     int storage = d->storage;
+    if (const char* e = std::getenv("NGPRT_STORAGE"))  // tuning override: "f32" | "f16" | "auto"
+        storage = std::strcmp(e, "f32") == 0 ? NGPRT_STORAGE_F32
+                  : std::strcmp(e, "f16") == 0 ? NGPRT_STORAGE_F16 : storage;
     if (storage == NGPRT_STORAGE_AUTO) {
         bool exact = true;
         for (uint64_t i = 0; exact && i < d->n_coarse * uint64_t(w); ++i)
@@ -451,8 +454,13 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
             const char* e = std::getenv("NGPRT_STEP_BURST");
             return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
         }();
+        static const int prefetch = [] {
+            const char* e = std::getenv("NGPRT_PREFETCH");
+            return e ? std::atoi(e) : 0;
+        }();
         p.decode_min = dmin;
         p.step_burst = burst;
+        p.prefetch = prefetch;
     }
     p.tiles_x = (W + 7) / 8;
     p.tiles_per_cam = p.tiles_x * ((H + 3) / 4);
