@@ -49,7 +49,17 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target wall time of the bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scene", action="append", default=[],
+                    help="override a synthetic-scene parameter, e.g. --scene n_boxes=560")
     return ap.parse_args()
+
+
+def scene_config(ng, args):
+    cfg = dict(ng.CONFIGS[args.config])
+    for kv in args.scene:
+        k, v = kv.split("=", 1)
+        cfg[k] = type(cfg.get(k, 0.0))(v) if k in cfg else (float(v) if "." in v else int(v))
+    return cfg
 
 
 def dist_env():
@@ -152,7 +162,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     import paper_2407_10482_b200 as ng
-    cfg = dict(ng.CONFIGS[args.config])
+    cfg = scene_config(ng, args)
     W, H = cfg["width"], cfg["height"]
     scene = ng.SynthScene(**cfg)
     cams = ng.cameras(N_CAMS, W, H)
@@ -198,7 +208,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = dict(ng.CONFIGS[args.config])
+    cfg = scene_config(ng, args)
     W, H = cfg["width"], cfg["height"]
     synth = ng.SynthScene(**cfg)
     scene = ng.Scene(synth, device=local)
@@ -294,9 +304,13 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": fps / PAPER_FPS,
             "dtype": "f32 (fp16 feature storage, lossless)", "data": "synthetic",
             "mrays_per_s": fps * W * H / 1e6,
-            "config": {"workload": f"{args.config}: {W}x{H} mip360-shaped synthetic scene, "
-                                   f"L={scene.L}, 2^21 entries/level, L_C=512, 512^3 pyramid, "
-                                   f"256^3 distance grid, mlp={args.mlp}",
+            "config": {"workload": (
+                f"{args.config}: {W}x{H} '{cfg['occupancy']}' synthetic scene"
+                + (f" ({cfg['n_boxes']} boxes)" if cfg['occupancy'] == 'boxes' else "")
+                + f", L={scene.L}, 2^{int(cfg['fine_table_len']).bit_length() - 1} entries/level, "
+                f"L_C={cfg['L_C']}, {cfg['occ_base_res']}^3 pyramid, "
+                f"{int(synth.desc.dist_res)}^3 distance grid, occupancy "
+                f"{100 * synth.occupancy_fraction():.2f}%, mlp={args.mlp}"),
                        "cameras": f"sphere_views({N_CAMS}, 2.9); rank r renders (r + N*step) % {N_CAMS}",
                        "l2": "flushed (256 MiB write) before every timed step" if not args.no_l2_flush
                              else "not flushed; scene (4.4 GB) larger than L2",

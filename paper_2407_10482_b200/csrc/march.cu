@@ -255,7 +255,8 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
 // + level_masked_fine (fusion.hpp:198-209) + fuse (fusion.hpp:107-173).
 // The weighted fuse adds level l's contribution right after that level is
 // interpolated; levels are visited in order, so every sum is formed in the
-// reference's order. `scr` is this thread's 8-float shared-memory scratch.
+// reference's order. `scr` is this thread's column of a [8][kBlock] shared
+// scratch (element j at scr[j * kBlock], so a warp's accesses hit 32 banks).
 template <int L, bool F16>
 __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3], int keep_level,
                                              const unsigned long long* tab, float* scr,
@@ -333,10 +334,18 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
     const bool variant = mode == NGPRT_FUSION_SEPARATE_ATT_V || mode == NGPRT_FUSION_SHARED_ATT_V;
     if (variant) {
 #pragma unroll
-        for (int j = 0; j < 2 * L; ++j) scr[j] = dec[8 + j];
+        for (int j = 0; j < 2 * L; ++j) scr[j * kBlock] = dec[8 + j];
         const int jstep = mode == NGPRT_FUSION_SHARED_ATT_V ? 2 : 1;
+        // two independent sigmoid chains per iteration (ILP across the expf latency)
 #pragma unroll 1
-        for (int j = 0; j < 2 * L; j += jstep) scr[j] = activate_sigmoid(scr[j], tab);
+        for (int j = 0; j < 2 * L; j += 2 * jstep) {
+            const int j2 = j + jstep;
+            const bool two = j2 < 2 * L;
+            const float y0 = activate_sigmoid(scr[j * kBlock], tab);
+            const float y1 = activate_sigmoid(two ? scr[j2 * kBlock] : 0.0f, tab);
+            scr[j * kBlock] = y0;
+            if (two) scr[j2 * kBlock] = y1;
+        }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) out[i] = dec[i];
@@ -351,8 +360,8 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
         }
         float wo, wb;
         if (variant) {
-            wo = scr[2 * l];
-            wb = mode == NGPRT_FUSION_SEPARATE_ATT_V ? scr[2 * l + 1] : wo;
+            wo = scr[2 * l * kBlock];
+            wb = mode == NGPRT_FUSION_SEPARATE_ATT_V ? scr[(2 * l + 1) * kBlock] : wo;
         } else if (mode == NGPRT_FUSION_SUM) {
             wo = wb = 1.0f;
         } else {
@@ -512,7 +521,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
     __shared__ float scratch[kBlock * 8];
     load_exp_table(tab);
     __syncthreads();
-    float* scr = scratch + threadIdx.x * 8;
+    float* scr = scratch + threadIdx.x;  // element j at scr[j * kBlock]: conflict-free banks
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned lt_mask = (1u << lane) - 1u;
     const uint32_t total_tiles = p.tiles_per_cam * uint32_t(p.n_cams);

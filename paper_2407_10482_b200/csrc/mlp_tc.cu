@@ -211,6 +211,14 @@ __global__ void __launch_bounds__(kThreads, 3)
         const bool shade = ray < n_rays && r.c.w != 0.f && r.a.w < 1.0f;
         const size_t nray = (tile + gridDim.x) * kM + tid;
         if (nray < n_rays) r_next = acc[nray];
+        if (!__syncthreads_or(shade)) {  // no ray of this tile is shaded: all black
+            if (ray < n_rays) {
+                rgb[3 * ray] = 0.f;
+                rgb[3 * ray + 1] = 0.f;
+                rgb[3 * ray + 2] = 0.f;
+            }
+            continue;
+        }
         // ---- layer 1 input row: [C_d, F, sh(dir)], zero-padded to K = 32 ----
         float x[kK1];
 #pragma unroll
