@@ -184,6 +184,20 @@ ngprt_status ngprt_test_hash_index(const int32_t* corners_dev, uint64_t n, uint3
                                    void* stream);
 
 /* ---------------------------------------------------------------------------
+ * The reference's baked-scene file (".ngrt", baking.hpp:229-485): magic "NGRT",
+ * version 1, header {L_C, L, fine_res[L], table_lens[6+L], fusion tag}, then
+ * CRC-32-checked sections 1 coarse map, 2 fine tables, 3 view MLP, 4 pyramid
+ * (512..32), 5 distance grid (256^3), 6 attention logits, 7 fusion MLP.
+ * ngprt_baked_load parses and validates on the host (errors carry the
+ * reference's messages and byte offsets); ngprt_scene_load uploads in one call.
+ * ------------------------------------------------------------------------- */
+typedef struct ngprt_baked ngprt_baked;
+ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out);
+const ngprt_scene_desc* ngprt_baked_desc(const ngprt_baked* b);
+void ngprt_baked_free(ngprt_baked* b);
+ngprt_status ngprt_scene_load(const char* path, int device, ngprt_scene** out);
+
+/* ---------------------------------------------------------------------------
  * Synthetic scenes (host-only input generation). Restates the reference's own
  * generators so the GPU and the CPU oracle consume the same scene object:
  * make_scene/scene_occupancy (scene.hpp:168-183,329-385), Rng (common.hpp:46-75),

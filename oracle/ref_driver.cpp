@@ -437,6 +437,17 @@ void ref_rng_uniform(uint64_t seed, double lo, double hi, uint64_t n, double* ou
 
 uint32_t ref_crc32(const void* p, uint64_t n) { return crc32(p, n); }
 
+// save_baked (baking.hpp:266-349) of a scene built by ref_scene_create.
+int ref_save_baked(void* handle, const char* path) {
+    try {
+        save_baked(static_cast<RefScene*>(handle)->s, path);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 double ref_base_step() { return kBaseStep; }
 
 } // extern "C"

@@ -141,6 +141,10 @@ SIGNATURES = {
     "ngprt_test_expf_range": (C.c_int, [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p]),
     "ngprt_test_hash_index": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint8,
                                         C.c_void_p, C.c_void_p]),
+    "ngprt_baked_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ngprt_baked_desc": (C.POINTER(SceneDesc), [C.c_void_p]),
+    "ngprt_baked_free": (None, [C.c_void_p]),
+    "ngprt_scene_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
     "ngprt_synth_default_params": (None, [C.POINTER(SynthParams)]),
     "ngprt_synth_create": (C.c_int, [C.POINTER(SynthParams), C.POINTER(C.c_void_p)]),
     "ngprt_synth_last_error": (C.c_char_p, []),

@@ -32,6 +32,7 @@ UNITS = [
     ("occupancy.cu", []),
     ("ngprt_abi.cu", []),
     ("synth.cpp", []),
+    ("ngrt_io.cpp", []),
 ]
 HEADERS = list(CSRC.glob("*.cuh")) + [INCLUDE / "ngprt_cuda.h"]
 

@@ -45,6 +45,10 @@ float host_sigmoid(float x) { return 1.0f / (1.0f + std::exp(-x)); }  // nn.hpp:
 
 }  // namespace
 
+namespace ngprt_host {
+void set_error(const std::string& msg) { g_err = msg; }  // used by the host-only units
+}
+
 struct ngprt_scene {
     int device = 0;
     DevScene ds{};

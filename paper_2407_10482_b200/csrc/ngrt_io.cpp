@@ -1,0 +1,220 @@
+// ngrt_io.cpp — host-side reader of the reference's baked-scene file format
+// (".ngrt", written by save_baked, read by load_baked: baking.hpp:229-485).
+//
+// Layout (little-endian): "NGRT", u32 version = 1, header { u32 L_C, u32 L,
+// u32 fine_res[L], u64 table_lens[6 + L], u8 fusion_tag, zero pad to an 8-byte
+// multiple }, then sections { u32 id, u64 byte_len, payload, u32 crc32(payload) }.
+// The parse mirrors load_baked's checks and error texts (with byte offsets) and
+// yields an ngprt_scene_desc whose pyramid levels and distance grid are the
+// file's own (512..32 and 256^3, baking.hpp:435-447).
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ngprt_cuda.h"
+
+namespace ngprt_host {
+void set_error(const std::string& msg);  // ngprt_abi.cu (ngprt_last_error)
+}
+
+struct ngprt_baked {
+    ngprt_scene_desc desc{};
+    std::vector<uint64_t> keys;
+    std::vector<float> rows;
+    std::vector<float> fine[NGPRT_MAX_FINE_LEVELS];
+    std::vector<float> psi_w[3], psi_b[3];
+    std::vector<float> att;
+    std::vector<uint64_t> pyramid[NGPRT_PYRAMID_LEVELS];
+    std::vector<uint8_t> dist;
+};
+
+namespace {
+
+constexpr uint32_t kVersion = 1;
+constexpr int kCoarseLevels = 6;
+
+struct Reader {  // detail::ByteReader, training.hpp:464-479
+    const unsigned char* p;
+    size_t len, off = 0;
+    void read(void* dst, size_t n, const char* what) {
+        if (off + n > len)
+            throw std::runtime_error(std::string("checkpoint: truncated reading ") + what +
+                                     " at offset " + std::to_string(off));
+        std::memcpy(dst, p + off, n);
+        off += n;
+    }
+    template <class V>
+    V pod(const char* what) {
+        V v;
+        read(&v, sizeof v, what);
+        return v;
+    }
+};
+
+void read_mlp(Reader& pr, const char* tag, std::vector<float>* w, std::vector<float>* b) {
+    const uint32_t nd = pr.pod<uint32_t>("mlp ndims");
+    std::vector<int> dims(nd);
+    for (auto& d : dims) d = int(pr.pod<uint32_t>("mlp dim"));
+    const std::vector<int> want = {23, 64, 64, 3};  // shade requires 23 -> 3 (volume.hpp:121-122)
+    if (dims != want)
+        throw std::runtime_error(std::string("load_baked: ") + tag +
+                                 " must be 23-64-64-3 (shade, volume.hpp:121-122)");
+    for (int k = 0; k < 3; ++k) {
+        w[k].resize(size_t(dims[k]) * dims[k + 1]);
+        b[k].resize(size_t(dims[k + 1]));
+        pr.read(w[k].data(), w[k].size() * 4, "mlp weights");
+        pr.read(b[k].data(), b[k].size() * 4, "mlp biases");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
+    if (!path || !out) {
+        ngprt_host::set_error("ngprt_baked_load: null argument");
+        return NGPRT_EINVAL;
+    }
+    *out = nullptr;
+    try {
+        std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "rb"), &std::fclose);
+        if (!f) throw std::runtime_error(std::string("load_baked: cannot open ") + path);
+        std::vector<unsigned char> buf;
+        unsigned char chunk[1 << 16];
+        size_t n;
+        while ((n = std::fread(chunk, 1, sizeof chunk, f.get())) > 0) buf.insert(buf.end(), chunk, chunk + n);
+        if (buf.size() < 8 || std::memcmp(buf.data(), "NGRT", 4) != 0)
+            throw std::runtime_error("load_baked: bad magic at offset 0");
+        Reader r{buf.data() + 4, buf.size() - 4};
+        if (r.pod<uint32_t>("version") != kVersion)
+            throw std::runtime_error("load_baked: unsupported version at offset 4");
+
+        auto b = std::make_unique<ngprt_baked>();
+        ngprt_scene_desc& d = b->desc;
+        const size_t header_start = r.off;
+        const uint32_t lc = r.pod<uint32_t>("L_C");
+        const uint32_t L = r.pod<uint32_t>("L");
+        if (L < 2 || L > 4) throw std::runtime_error("load_baked: L out of range");
+        d.L = L;
+        d.L_C = lc;
+        for (uint32_t l = 0; l < L; ++l) d.fine_res[l] = r.pod<uint32_t>("fine resolution");
+        std::vector<uint64_t> lens(kCoarseLevels + L);
+        for (auto& v : lens) v = r.pod<uint64_t>("table length");
+        for (uint32_t l = 0; l < L; ++l) {
+            d.fine_table_len[l] = lens[kCoarseLevels + l];
+            d.fine_hashed[l] = 1;  // load_baked: Addressing::Hashed (baking.hpp:384)
+        }
+        d.fusion_tag = r.pod<uint8_t>("fusion tag");
+        while ((r.off - header_start) % 8 != 0) r.pod<uint8_t>("pad");
+        const int w = 8 + 2 * int(L);
+
+        bool saw[8] = {};
+        while (r.off < r.len) {
+            const size_t sec_off = r.off;
+            const uint32_t id = r.pod<uint32_t>("section id");
+            const uint64_t len = r.pod<uint64_t>("section length");
+            if (r.off + len + 4 > r.len)
+                throw std::runtime_error("load_baked: truncated section " + std::to_string(id) +
+                                         " at offset " + std::to_string(sec_off));
+            const unsigned char* payload = r.p + r.off;
+            r.off += len;
+            const uint32_t crc = r.pod<uint32_t>("section crc");
+            if (ngprt_crc32(payload, len, 0) != crc)
+                throw std::runtime_error("load_baked: checksum failure in section " +
+                                         std::to_string(id) + " at offset " +
+                                         std::to_string(sec_off));
+            Reader pr{payload, len};
+            switch (id) {
+                case 1: {  // coarse corner map, sorted by key
+                    const uint64_t count = pr.pod<uint64_t>("corner count");
+                    b->keys.resize(count);
+                    b->rows.resize(count * w);
+                    for (uint64_t i = 0; i < count; ++i) {
+                        b->keys[i] = pr.pod<uint64_t>("corner index");
+                        pr.read(b->rows.data() + i * w, sizeof(float) * w, "corner row");
+                    }
+                    break;
+                }
+                case 2:
+                    for (uint32_t l = 0; l < L; ++l) {
+                        b->fine[l].resize(d.fine_table_len[l] * 8);
+                        pr.read(b->fine[l].data(), b->fine[l].size() * 4, "fine table");
+                    }
+                    break;
+                case 3:
+                    read_mlp(pr, "view MLP", b->psi_w, b->psi_b);
+                    break;
+                case 4:
+                    for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) {
+                        const size_t res = size_t(512) >> k;
+                        b->pyramid[k].resize((res * res * res + 63) / 64);
+                        pr.read(b->pyramid[k].data(), b->pyramid[k].size() * 8, "pyramid");
+                    }
+                    break;
+                case 5:
+                    b->dist.resize(size_t(256) * 256 * 256);
+                    pr.read(b->dist.data(), b->dist.size(), "distance grid");
+                    break;
+                case 6:
+                    b->att.resize(size_t(2) * L);
+                    pr.read(b->att.data(), b->att.size() * 4, "attention globals");
+                    break;
+                case 7:
+                    throw std::runtime_error(
+                        "load_baked: fusion MLP section (ablation mode 'mlp') is not supported by "
+                        "this renderer");
+                default:
+                    throw std::runtime_error("load_baked: unknown section id " + std::to_string(id) +
+                                             " at offset " + std::to_string(sec_off));
+            }
+            if (pr.off != pr.len)
+                throw std::runtime_error("load_baked: section " + std::to_string(id) +
+                                         " length mismatch at offset " + std::to_string(sec_off));
+            if (id <= 7) saw[id] = true;
+        }
+        for (uint32_t id : {1u, 2u, 3u, 4u, 5u})
+            if (!saw[id]) throw std::runtime_error("load_baked: missing section " + std::to_string(id));
+        const bool inv = d.fusion_tag == NGPRT_FUSION_SHARED_ATT_INV ||
+                         d.fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV;
+        if (inv && !saw[6]) throw std::runtime_error("load_baked: missing attention globals section");
+
+        d.n_coarse = b->keys.size();
+        d.coarse_keys = b->keys.data();
+        d.coarse_rows = b->rows.data();
+        for (uint32_t l = 0; l < L; ++l) d.fine_tables[l] = b->fine[l].data();
+        for (int k = 0; k < 3; ++k) {
+            d.psi_w[k] = b->psi_w[k].data();
+            d.psi_b[k] = b->psi_b[k].data();
+        }
+        d.att_globals = b->att.empty() ? nullptr : b->att.data();
+        d.occ_base_res = 512;
+        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) d.pyramid_words[k] = b->pyramid[k].data();
+        d.dist_res = 256;
+        d.dist_values = b->dist.data();
+        d.storage = NGPRT_STORAGE_AUTO;
+        *out = b.release();
+        return NGPRT_OK;
+    } catch (const std::exception& e) {
+        ngprt_host::set_error(e.what());
+        return NGPRT_EINVAL;
+    }
+}
+
+const ngprt_scene_desc* ngprt_baked_desc(const ngprt_baked* b) { return b ? &b->desc : nullptr; }
+
+void ngprt_baked_free(ngprt_baked* b) { delete b; }
+
+ngprt_status ngprt_scene_load(const char* path, int device, ngprt_scene** out) {
+    ngprt_baked* b = nullptr;
+    ngprt_status st = ngprt_baked_load(path, &b);
+    if (st != NGPRT_OK) return st;
+    st = ngprt_scene_create(&b->desc, device, out);
+    ngprt_baked_free(b);
+    return st;
+}
+
+}  // extern "C"

@@ -125,6 +125,31 @@ class SynthScene:
         self.close()
 
 
+class BakedFile:
+    """A baked scene read from the reference's `.ngrt` file (load_baked,
+    baking.hpp:351-485) on the host: CRC-checked sections, the file's own
+    512..32 pyramid and 256^3 distance grid. Pass it to Scene() to upload."""
+
+    def __init__(self, path):
+        h = C.c_void_p()
+        check(lib().ngprt_baked_load(str(path).encode(), C.byref(h)), "ngprt_baked_load")
+        self._h = h
+        self.desc_ptr = lib().ngprt_baked_desc(h)
+        self.desc: SceneDesc = self.desc_ptr.contents
+
+    @property
+    def L(self):
+        return int(self.desc.L)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ngprt_baked_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
 def cameras(n: int, width: int, height: int, radius: float = 2.9):
     """sphere_views(n, radius) with synth_dataset intrinsics (scene.hpp:254-265, 388-395)."""
     cams = (Camera * n)()
@@ -175,8 +200,8 @@ class Scene:
     """A BakedScene resident on one B200 (ngprt_scene). Immutable after creation."""
 
     def __init__(self, desc, device: int = 0, storage: int = _abi.STORAGE_AUTO):
-        if isinstance(desc, SynthScene):
-            self._synth = desc  # keep host arrays alive for the call
+        if hasattr(desc, "desc_ptr"):  # SynthScene / BakedFile: keep host arrays alive
+            self._synth = desc
             desc_ptr = desc.desc_ptr
         else:
             desc_ptr = C.pointer(desc)

@@ -114,6 +114,8 @@ def ref():
         L.ref_crc32.restype = C.c_uint32
         L.ref_crc32.argtypes = [P, C.c_uint64]
         L.ref_base_step.restype = C.c_double
+        L.ref_save_baked.restype = C.c_int
+        L.ref_save_baked.argtypes = [P, C.c_char_p]
         _ref = L
     return _ref
 

@@ -1,0 +1,96 @@
+"""The reference's baked-scene file (.ngrt, baking.hpp:229-485) as input.
+
+CPU: a scene saved by the reference's own save_baked is read back by
+ngprt_baked_load bit for bit (every section), and corrupt/truncated files fail
+with the reference's error texts. GPU: the loaded file renders bit-exactly like
+the reference renders the same BakedScene."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from checkers import CpuScene, ref
+
+SCENE = dict(occupancy="toy", occ_base_res=512, L=2, L_C=64, fine_table_len=1 << 12,
+             fusion_tag="separate_att_inv")
+
+
+@pytest.fixture(scope="module")
+def saved(tmp_path_factory, ng):
+    R = ref()
+    if R is None:
+        pytest.skip("compiled reference (oracle/_ref) not available")
+    synth = ng.SynthScene(**SCENE)
+    rs = CpuScene(synth.desc_ptr, "ref")
+    path = tmp_path_factory.mktemp("ngrt") / "scene.ngrt"
+    assert R.ref_save_baked(rs.h, str(path).encode()) == 0
+    return synth, rs, path
+
+
+def _arr(ptr, n, dt):
+    import ctypes as C
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), shape=(n,))
+
+
+def test_load_matches_saved_scene(ng, saved):
+    synth, _, path = saved
+    b = ng.BakedFile(path)
+    d, s = b.desc, synth.desc
+    assert (d.L, d.L_C, d.fusion_tag) == (s.L, s.L_C, s.fusion_tag)
+    assert list(d.fine_res)[: d.L] == list(s.fine_res)[: s.L]
+    assert list(d.fine_table_len)[: d.L] == list(s.fine_table_len)[: s.L]
+    # coarse map: the file is sorted by key (baking.hpp:288-291); compare as sets of rows
+    w = 8 + 2 * d.L
+    ks, rs = synth.coarse_keys(), synth.coarse_rows()
+    kf = _arr(d.coarse_keys, d.n_coarse, np.uint64)
+    rf = _arr(d.coarse_rows, d.n_coarse * w, np.float32).reshape(-1, w)
+    order = np.argsort(ks)
+    assert np.array_equal(kf, ks[order])
+    assert np.array_equal(rf.view(np.uint32), rs[order].view(np.uint32))
+    for l in range(d.L):
+        n = int(d.fine_table_len[l]) * 8
+        assert np.array_equal(_arr(d.fine_tables[l], n, np.float32), synth.fine_table(l).ravel())
+    ws, bs = synth.psi()
+    for k, (wk, bk) in enumerate(zip(ws, bs)):
+        assert np.array_equal(_arr(d.psi_w[k], wk.size, np.float32), wk.ravel())
+        assert np.array_equal(_arr(d.psi_b[k], bk.size, np.float32), bk)
+    assert np.array_equal(_arr(d.att_globals, 2 * d.L, np.float32),
+                          _arr(s.att_globals, 2 * s.L, np.float32))
+    # pyramid level 0 is the scene's occupancy; levels 1..4 / distance grid are the reference's
+    assert np.array_equal(_arr(d.pyramid_words[0], 512 ** 3 // 64, np.uint64), synth.base_words())
+    assert d.occ_base_res == 512 and d.dist_res == 256
+
+
+def test_corrupt_files_fail_like_the_reference(ng, saved, tmp_path):
+    _, _, path = saved
+    data = bytearray(path.read_bytes())
+    bad_magic = tmp_path / "magic.ngrt"
+    bad_magic.write_bytes(b"XXXX" + bytes(data[4:]))
+    with pytest.raises(ng.NgprtError, match="bad magic at offset 0"):
+        ng.BakedFile(bad_magic)
+    flipped = bytearray(data)
+    flipped[len(flipped) // 2] ^= 0xFF
+    p = tmp_path / "flip.ngrt"
+    p.write_bytes(bytes(flipped))
+    with pytest.raises(ng.NgprtError, match="checksum failure in section"):
+        ng.BakedFile(p)
+    p2 = tmp_path / "trunc.ngrt"
+    p2.write_bytes(bytes(data[: len(data) - 100]))
+    with pytest.raises(ng.NgprtError, match="truncated section"):
+        ng.BakedFile(p2)
+    with pytest.raises(ng.NgprtError, match="cannot open"):
+        ng.BakedFile(tmp_path / "missing.ngrt")
+
+
+@pytest.mark.gpu
+def test_loaded_file_renders_like_the_reference(ng, saved):
+    import torch
+    _, rs, path = saved
+    dev = ng.Scene(ng.BakedFile(path))
+    cam = ng.cameras(4, 48, 40)[1]
+    opts = ng.Opts(mlp="exact")
+    rgb, st = ng.render(dev, [cam], opts, stats=True)
+    torch.cuda.synchronize()
+    want_rgb, want_st = rs.render(cam, opts.to_c(), nthreads=8)
+    assert np.array_equal(st[0].cpu().numpy().view(np.uint32), want_st)
+    assert np.array_equal(rgb[0].cpu().numpy().view(np.uint32), want_rgb.view(np.uint32))
