@@ -57,7 +57,7 @@ typedef enum {
     NGPRT_FUSION_SEPARATE_ATT_INV = 2,
     NGPRT_FUSION_SHARED_ATT_V = 3,
     NGPRT_FUSION_SEPARATE_ATT_V = 4,
-    NGPRT_FUSION_MLP = 5 /* ablation only (PAPER Table 3); rejected with NGPRT_EUNSUPPORTED */
+    NGPRT_FUSION_MLP = 5 /* ablation (PAPER Table 3): fine features through an {8L,64,8} MLP */
 } ngprt_fusion_tag;
 
 /* How feature rows are stored in HBM. AUTO picks fp16 when every coarse row
@@ -94,6 +94,8 @@ typedef struct ngprt_scene_desc {
     const uint64_t* pyramid_words[NGPRT_PYRAMID_LEVELS]; /* [0] required; [1..4] NULL => built on device */
     const uint8_t* dist_values;                  /* dist_res^3, NULL => built on device from the
                                                     pyramid level whose res == dist_res       */
+    const float* fusion_mlp_w[2];                /* FusionMode::mlp {8L, 64, 8} (MLP mode only): */
+    const float* fusion_mlp_b[2];                /* W0 64 x 8L, b0 64, W1 8 x 64, b1 8       */
 } ngprt_scene_desc;
 
 /* Pinhole camera: PosedDataset intrinsics + one Frame (scene.hpp:191-201).

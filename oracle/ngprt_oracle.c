@@ -335,6 +335,15 @@ void orc_decode_point(const orc_scene* s, const float* x, int keep_level, float*
         for (int l = 0; l < L; ++l)
             if (l + 1 != keep_level)
                 for (int ch = 1; ch < 8; ++ch) fine[l][ch] = 0.0f;
+    if (s->d.fusion_tag == NGPRT_FUSION_MLP) { /* fuse, MLP ablation: fusion.hpp:162-171 */
+        float in[32], hat[8];
+        for (int l = 0; l < L; ++l)
+            for (int ch = 0; ch < 8; ++ch) in[8 * l + ch] = fine[l][ch];
+        const int widths[3] = {8 * L, 64, 8};
+        orc_mlp_forward(2, widths, s->d.fusion_mlp_w, s->d.fusion_mlp_b, in, hat);
+        for (int i = 0; i < 8; ++i) out[i] = dec[i] + hat[i];
+        return;
+    }
     float wo[4], wb[4];
     for (int l = 0; l < L; ++l) {
         switch (s->d.fusion_tag) {

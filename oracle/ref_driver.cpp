@@ -96,6 +96,13 @@ void* ref_scene_create(const ngprt_scene_desc* d) {
         s.fusion.init(s.tag, L, dummy, nullptr);
         if (fusion_is_invariant(s.tag))
             for (int i = 0; i < 2 * L; ++i) s.fusion.global_pre.value[i] = d->att_globals[i];
+        if (s.tag == FusionTag::Mlp)
+            for (int k = 0; k < 2; ++k) {
+                std::memcpy(s.fusion.mlp.weight[k].value.data(), d->fusion_mlp_w[k],
+                            sizeof(float) * s.fusion.mlp.weight[k].value.size());
+                std::memcpy(s.fusion.mlp.bias[k].value.data(), d->fusion_mlp_b[k],
+                            sizeof(float) * s.fusion.mlp.bias[k].value.size());
+            }
         // The reference's own pyramid and distance transform, from level 0 only.
         s.pyramid = build_pyramid(bitgrid_from_words(d->pyramid_words[0], int(d->occ_base_res)));
         if (d->dist_res) {

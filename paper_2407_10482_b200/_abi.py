@@ -44,6 +44,8 @@ class SceneDesc(C.Structure):
         ("dist_res", C.c_uint32),
         ("pyramid_words", C.POINTER(C.c_uint64) * PYRAMID_LEVELS),
         ("dist_values", C.POINTER(C.c_uint8)),
+        ("fusion_mlp_w", C.POINTER(C.c_float) * 2),
+        ("fusion_mlp_b", C.POINTER(C.c_float) * 2),
     ]
 
 

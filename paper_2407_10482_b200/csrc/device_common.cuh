@@ -123,6 +123,7 @@ struct DevScene {
     int dist_res;
     const uint8_t* dist;
     const float* psi;     // packed f32 weights: W0 (64x23) b0 W1 (64x64) b1 W2 (3x64) b2
+    const float* fmlp;    // MLP fusion {8L,64,8}: W0 (64x8L) b0 (64) W1 (8x64) b1 (8), or null
 
     // ---- derived constants (ngprt_scene_create); each equals the float the
     // reference computes at that point, so using them is bit-exact ----

@@ -255,35 +255,14 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
 // + level_masked_fine (fusion.hpp:198-209) + fuse (fusion.hpp:107-173).
 // The weighted fuse adds level l's contribution right after that level is
 // interpolated; levels are visited in order, so every sum is formed in the
-// reference's order. `scr` is this thread's column of a [8][kBlock] shared
+// reference's order. `scr` is this thread's column of a [rows][kBlock] shared
 // scratch (element j at scr[j * kBlock], so a warp's accesses hit 32 banks).
-template <int L, bool F16>
+// MLPF: the MLP-fusion ablation (fusion.hpp:162-171) instead of attention.
+template <int L, bool F16, bool MLPF>
 __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3], int keep_level,
                                              const unsigned long long* tab, float* scr,
-                                             int prefetch, float out[8]) {
+                                             float out[8]) {
     constexpr int W = 8 + 2 * L;
-    if (prefetch) {
-        // The fine rows depend only on x: pull them towards L1 now so the
-        // per-level loads below do not add two more dependent L2 round trips.
-#pragma unroll 1
-        for (int l = 0; l < L; ++l) {
-            if (sc.fine_mode[l] != 1) continue;
-            int b[3];
-            float f[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[l], sc.fine_res[l], b[a], f[a]);
-            const uint32_t mask = sc.fine_mask[l];
-            const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
-            const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
-            const char* base = static_cast<const char*>(sc.fine[l]);
-            const int rb = F16 ? 16 : 32;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t idx = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
-                asm volatile("prefetch.global.L1 [%0];" :: "l"(base + size_t(idx) * rb));
-            }
-        }
-    }
     // coarse: stencil at L_C, 8 corner rows, interpolation in corner order
     // k = 0..7 from a zero start (baking.hpp:72-78; absent corners are zero rows)
     float dec[W];
@@ -327,6 +306,52 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
                 for (int i = 0; i < W; ++i) dec[i] += wk * row[i];
             }
         }
+    }
+    if constexpr (MLPF) {
+        // fuse, MLP mode (fusion.hpp:162-171): concatenated (masked) fine features
+        // through TinyMlp {8L, 64, 8} (nn.hpp:175-196), added to the coarse feature.
+        constexpr int IN = 8 * L;
+#pragma unroll 1
+        for (int l = 0; l < L; ++l) {
+            float fine[8];
+            fine_level<F16>(sc, l, x, fine);
+            if (keep_level > 0 && l + 1 != keep_level) {
+#pragma unroll
+                for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) scr[(8 * l + c) * kBlock] = fine[c];
+        }
+        float in[IN];
+#pragma unroll
+        for (int c = 0; c < IN; ++c) in[c] = scr[c * kBlock];
+        const float* W0 = sc.fmlp;
+        const float* B0 = W0 + 64 * IN;
+        const float* W1 = B0 + 64;
+        const float* B1 = W1 + 8 * 64;
+        float hat[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hat[j] = __ldg(B1 + j);
+        // hidden unit by unit; the output layer accumulates in the reference's c-order
+#pragma unroll 1
+        for (int r = 0; r < 64; ++r) {
+            float h = __ldg(B0 + r);
+            const float4* wr = reinterpret_cast<const float4*>(W0 + r * IN);
+#pragma unroll
+            for (int q = 0; q < IN / 4; ++q) {
+                const float4 wq = __ldg(wr + q);
+                h += wq.x * in[4 * q];
+                h += wq.y * in[4 * q + 1];
+                h += wq.z * in[4 * q + 2];
+                h += wq.w * in[4 * q + 3];
+            }
+            h = h < 0.0f ? 0.0f : h;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hat[j] += __ldg(W1 + j * 64 + r) * h;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = dec[i] + hat[i];
+        return;
     }
     // post-sigmoid attention (split_decoder_output, model.hpp:18-21) for the
     // spatially variant modes: one sigmoid loop over the 2L logits in scratch
@@ -514,11 +539,11 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     return true;
 }
 
-template <int L, bool F16>
+template <int L, bool F16, bool MLPF>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScene sc,
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
-    __shared__ float scratch[kBlock * 8];
+    __shared__ float scratch[kBlock * (MLPF ? 8 * L : 8)];
     load_exp_table(tab);
     __syncthreads();
     float* scr = scratch + threadIdx.x;  // element j at scr[j * kBlock]: conflict-free banks
@@ -566,7 +591,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             // ---- decode phase: emit(t) of the canonical render_ray ----
             if (s.has_ray && s.pending) {
                 float f[8];
-                decode_point<L, F16>(sc, s.xc, p.keep_level, tab, scr, p.prefetch, f);
+                decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
                 // composite, volume.hpp:61-70
                 const float sigma = activate_density(f[0], tab);
                 const float a = alpha_from_sigma(sigma, step, tab);
@@ -627,26 +652,36 @@ __global__ void __launch_bounds__(256) raygen_kernel(const MarchParams p) {
     if (p.stats) p.stats[idx] = ngprt_ray_stats{0u, 0u, 0u, 0u};
 }
 
-template <int L, bool F16>
+template <int L, bool F16, bool MLPF>
 int ctas_per_sm_t() {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<L, F16>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<L, F16, MLPF>, kBlock, 0);
     return n > 0 ? n : 1;
 }
 
-template <int L, bool F16>
+template <int L, bool F16, bool MLPF>
 void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
     static int grid = 0;
     if (!grid) {
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = sms * ctas_per_sm_t<L, F16>();
+        grid = sms * ctas_per_sm_t<L, F16, MLPF>();
     }
     raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
     const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);
     const uint32_t need = (tiles + 3) / 4;  // 4 warps per CTA
-    march_kernel<L, F16><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
+    march_kernel<L, F16, MLPF><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
+}
+
+template <int L>
+void launch_l(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
+    const bool f16 = sc.storage == NGPRT_STORAGE_F16, mlp = sc.fusion == NGPRT_FUSION_MLP;
+    if (mlp) {
+        f16 ? launch_t<L, true, true>(sc, p, st) : launch_t<L, false, true>(sc, p, st);
+    } else {
+        f16 ? launch_t<L, true, false>(sc, p, st) : launch_t<L, false, false>(sc, p, st);
+    }
 }
 
 // Probe codes (see DevScene::probe).
@@ -672,22 +707,21 @@ __global__ void probe_code_kernel(const DevScene sc, uint16_t* __restrict__ out)
 }  // namespace
 
 void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
-    const bool f16 = sc.storage == NGPRT_STORAGE_F16;
     switch (sc.L) {
-        case 1: f16 ? launch_t<1, true>(sc, p, st) : launch_t<1, false>(sc, p, st); break;
-        case 2: f16 ? launch_t<2, true>(sc, p, st) : launch_t<2, false>(sc, p, st); break;
-        case 3: f16 ? launch_t<3, true>(sc, p, st) : launch_t<3, false>(sc, p, st); break;
-        default: f16 ? launch_t<4, true>(sc, p, st) : launch_t<4, false>(sc, p, st); break;
+        case 1: launch_l<1>(sc, p, st); break;
+        case 2: launch_l<2>(sc, p, st); break;
+        case 3: launch_l<3>(sc, p, st); break;
+        default: launch_l<4>(sc, p, st); break;
     }
 }
 
 int march_ctas_per_sm(const DevScene& sc) {
     const bool f16 = sc.storage == NGPRT_STORAGE_F16;
     switch (sc.L) {
-        case 1: return f16 ? ctas_per_sm_t<1, true>() : ctas_per_sm_t<1, false>();
-        case 2: return f16 ? ctas_per_sm_t<2, true>() : ctas_per_sm_t<2, false>();
-        case 3: return f16 ? ctas_per_sm_t<3, true>() : ctas_per_sm_t<3, false>();
-        default: return f16 ? ctas_per_sm_t<4, true>() : ctas_per_sm_t<4, false>();
+        case 1: return f16 ? ctas_per_sm_t<1, true, false>() : ctas_per_sm_t<1, false, false>();
+        case 2: return f16 ? ctas_per_sm_t<2, true, false>() : ctas_per_sm_t<2, false, false>();
+        case 3: return f16 ? ctas_per_sm_t<3, true, false>() : ctas_per_sm_t<3, false, false>();
+        default: return f16 ? ctas_per_sm_t<4, true, false>() : ctas_per_sm_t<4, false, false>();
     }
 }
 

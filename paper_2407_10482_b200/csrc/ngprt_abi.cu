@@ -104,10 +104,10 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
     if (d->L < 1 || d->L > NGPRT_MAX_FINE_LEVELS)
         return fail(NGPRT_EINVAL, "L out of range (1..4; the reference accepts 2..4, baking.hpp:366)");
     if (d->L_C < 1) return fail(NGPRT_EINVAL, "L_C must be >= 1");
-    if (d->fusion_tag == NGPRT_FUSION_MLP)
-        return fail(NGPRT_EUNSUPPORTED,
-                    "fusion mode 'mlp' (ablation, fusion.hpp:162-171) is not implemented");
     if (d->fusion_tag > NGPRT_FUSION_MLP) return fail(NGPRT_EINVAL, "unknown fusion tag");
+    if (d->fusion_tag == NGPRT_FUSION_MLP &&
+        !(d->fusion_mlp_w[0] && d->fusion_mlp_w[1] && d->fusion_mlp_b[0] && d->fusion_mlp_b[1]))
+        return fail(NGPRT_EINVAL, "fusion mode 'mlp' needs the {8L,64,8} fusion MLP (baking.hpp:482)");
     if ((d->fusion_tag == NGPRT_FUSION_SHARED_ATT_INV ||
          d->fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV) &&
         !d->att_globals)
@@ -358,6 +358,21 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         NG_TRY(cudaMemcpyAsync(s->psi_tc, tc.data(), tc.size(), cudaMemcpyHostToDevice, st));
         NG_TRY(cudaStreamSynchronize(st));
     }
+    // --- MLP-fusion ablation weights {8L,64,8}, packed f32 (fusion.hpp:91,162-171) ---
+    ds.fmlp = nullptr;
+    if (d->fusion_tag == NGPRT_FUSION_MLP) {
+        const size_t in = size_t(8) * L;
+        std::vector<float> packed(64 * in + 64 + 8 * 64 + 8);
+        std::memcpy(packed.data(), d->fusion_mlp_w[0], 64 * in * 4);
+        std::memcpy(packed.data() + 64 * in, d->fusion_mlp_b[0], 64 * 4);
+        std::memcpy(packed.data() + 64 * in + 64, d->fusion_mlp_w[1], 8 * 64 * 4);
+        std::memcpy(packed.data() + 64 * in + 64 + 8 * 64, d->fusion_mlp_b[1], 8 * 4);
+        float* g;
+        NG_TRY(s->alloc(&g, packed.size() * 4));
+        NG_TRY(cudaMemcpyAsync(g, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice, st));
+        NG_TRY(cudaStreamSynchronize(st));
+        ds.fmlp = g;
+    }
     // --- invariant attention weights: activate_sigmoid(global_pre) (fusion.hpp:123-132) ---
     if (d->fusion_tag == NGPRT_FUSION_SHARED_ATT_INV || d->fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV)
         for (int i = 0; i < 2 * L; ++i) ds.att_w[i] = host_sigmoid(d->att_globals[i]);
@@ -458,13 +473,8 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
             const char* e = std::getenv("NGPRT_STEP_BURST");
             return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
         }();
-        static const int prefetch = [] {
-            const char* e = std::getenv("NGPRT_PREFETCH");
-            return e ? std::atoi(e) : 0;
-        }();
         p.decode_min = dmin;
         p.step_burst = burst;
-        p.prefetch = prefetch;
     }
     p.tiles_x = (W + 7) / 8;
     p.tiles_per_cam = p.tiles_x * ((H + 3) / 4);

@@ -27,6 +27,7 @@ struct ngprt_baked {
     std::vector<float> fine[NGPRT_MAX_FINE_LEVELS];
     std::vector<float> psi_w[3], psi_b[3];
     std::vector<float> att;
+    std::vector<float> fmlp_w[2], fmlp_b[2];
     std::vector<uint64_t> pyramid[NGPRT_PYRAMID_LEVELS];
     std::vector<uint8_t> dist;
 };
@@ -163,10 +164,20 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
                     b->att.resize(size_t(2) * L);
                     pr.read(b->att.data(), b->att.size() * 4, "attention globals");
                     break;
-                case 7:
-                    throw std::runtime_error(
-                        "load_baked: fusion MLP section (ablation mode 'mlp') is not supported by "
-                        "this renderer");
+                case 7: {  // fusion MLP {8L, 64, 8} (baking.hpp:452-466)
+                    const uint32_t nd = pr.pod<uint32_t>("fusion mlp ndims");
+                    std::vector<int> dims(nd);
+                    for (auto& dd : dims) dd = int(pr.pod<uint32_t>("fusion mlp dim"));
+                    if (dims != std::vector<int>{8 * int(L), 64, 8})
+                        throw std::runtime_error("load_baked: fusion MLP must be 8L-64-8 (fusion.hpp:101)");
+                    for (int k = 0; k < 2; ++k) {
+                        b->fmlp_w[k].resize(size_t(dims[k]) * dims[k + 1]);
+                        b->fmlp_b[k].resize(size_t(dims[k + 1]));
+                        pr.read(b->fmlp_w[k].data(), b->fmlp_w[k].size() * 4, "fusion mlp weights");
+                        pr.read(b->fmlp_b[k].data(), b->fmlp_b[k].size() * 4, "fusion mlp biases");
+                    }
+                    break;
+                }
                 default:
                     throw std::runtime_error("load_baked: unknown section id " + std::to_string(id) +
                                              " at offset " + std::to_string(sec_off));
@@ -181,6 +192,12 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
         const bool inv = d.fusion_tag == NGPRT_FUSION_SHARED_ATT_INV ||
                          d.fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV;
         if (inv && !saw[6]) throw std::runtime_error("load_baked: missing attention globals section");
+        if (d.fusion_tag == NGPRT_FUSION_MLP && !saw[7])
+            throw std::runtime_error("load_baked: missing fusion MLP section");
+        for (int k = 0; k < 2; ++k) {
+            d.fusion_mlp_w[k] = b->fmlp_w[k].empty() ? nullptr : b->fmlp_w[k].data();
+            d.fusion_mlp_b[k] = b->fmlp_b[k].empty() ? nullptr : b->fmlp_b[k].data();
+        }
 
         d.n_coarse = b->keys.size();
         d.coarse_keys = b->keys.data();

@@ -23,7 +23,6 @@ struct MarchParams {
     float step;
     int use_grid, max_step_rule, early_stop, keep_level;
     int decode_min, step_burst;  // K1 warp scheduling policy (tunable, see march.cu)
-    int prefetch;                // L1-prefetch the fine rows at decode start
     RayAcc* acc;              // n_cams x h x w
     ngprt_ray_stats* stats;   // nullable, n_cams x h x w
     unsigned int* work;       // tile counter (zeroed before launch)

@@ -227,6 +227,7 @@ struct ngprt_synth {
     std::vector<float> fine[NGPRT_MAX_FINE_LEVELS];
     std::vector<float> psi_w[3], psi_b[3];
     std::vector<float> att;
+    std::vector<float> fmlp_w[2], fmlp_b[2];
 };
 
 extern "C" {
@@ -327,6 +328,21 @@ ngprt_status ngprt_synth_create(const ngprt_synth_params* p, ngprt_synth** out) 
                 for (auto& v : s->psi_b[k])
                     v = rnd(float(brng.uniform(-p->psi_bias_scale, p->psi_bias_scale)));
         }
+        // MLP-fusion ablation: FusionMode::mlp = TinyMlp::init({8L, 64, 8}) (fusion.hpp:101)
+        if (p->fusion_tag == NGPRT_FUSION_MLP) {
+            const int fw[3] = {8 * L, 64, 8};
+            Rng mrng(p->psi_seed + 2);
+            for (int k = 0; k < 2; ++k) {
+                const int in = fw[k], o = fw[k + 1];
+                const double bound = (k + 1 < 2) ? std::sqrt(6.0 / in) : std::sqrt(6.0 / (in + o));
+                s->fmlp_w[k].resize(size_t(in) * o);
+                for (auto& v : s->fmlp_w[k]) v = rnd(float(mrng.uniform(-bound, bound)));
+                s->fmlp_b[k].assign(size_t(o), 0.f);
+                if (p->psi_bias_scale > 0)
+                    for (auto& v : s->fmlp_b[k])
+                        v = rnd(float(mrng.uniform(-p->psi_bias_scale, p->psi_bias_scale)));
+            }
+        }
         // Global attention logits (invariant fusion modes only).
         Rng arng(p->coarse_seed + 0x5bd1e995ull);
         s->att.resize(size_t(2) * L);
@@ -346,6 +362,10 @@ ngprt_status ngprt_synth_create(const ngprt_synth_params* p, ngprt_synth** out) 
             d.psi_b[k] = s->psi_b[k].data();
         }
         d.att_globals = s->att.data();
+        for (int k = 0; k < 2; ++k) {
+            d.fusion_mlp_w[k] = s->fmlp_w[k].empty() ? nullptr : s->fmlp_w[k].data();
+            d.fusion_mlp_b[k] = s->fmlp_b[k].empty() ? nullptr : s->fmlp_b[k].data();
+        }
         d.occ_base_res = p->occ_base_res;
         d.pyramid_words[0] = s->base_words.data();
         d.dist_res = p->dist_level < NGPRT_PYRAMID_LEVELS ? (p->occ_base_res >> p->dist_level) : 0;

@@ -42,6 +42,13 @@ CASES = [
     dict(name="nonpow2_table_step2", scene=dict(occupancy="toy", occ_base_res=64, L=2, L_C=64,
                                                 fine_table_len=3001),
          cam=dict(w=48, h=48, n=4, i=3), opts=dict(step=2 * K_BASE_STEP)),
+    dict(name="mlp_fusion_l2", scene=dict(occupancy="bench", occ_base_res=128, L=2, L_C=128,
+                                          fine_table_len=1 << 14, fusion_tag="mlp",
+                                          psi_bias_scale=0.1),
+         cam=dict(w=48, h=48, n=4, i=0), opts=dict()),
+    dict(name="mlp_fusion_l4_keep3", scene=dict(occupancy="toy", occ_base_res=64, L=4, L_C=64,
+                                                fine_table_len=1 << 12, fusion_tag="mlp"),
+         cam=dict(w=40, h=40, n=4, i=2), opts=dict(keep_level=3)),
     dict(name="mip360_window", scene=dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
                                           fine_table_len=1 << 21, sigma_lo=1.0, sigma_hi=4.0),
          cam=dict(w=1920, h=1080, n=1, i=0), opts=dict(window=(928, 508, 64, 64))),

@@ -249,6 +249,6 @@ def test_errors_are_reported(ng, torch):
         ng.render(dev, [cam], ng.Opts(keep_level=3))
     with pytest.raises(ng.NgprtError, match="out of bounds"):
         ng.render(dev, [cam], ng.Opts(window=(10, 10, 8, 8)))
-    scene.desc.fusion_tag = 5
-    with pytest.raises(ng.NgprtError, match="EUNSUPPORTED"):
+    scene.desc.fusion_tag = 5  # MLP fusion without its {8L,64,8} weights
+    with pytest.raises(ng.NgprtError, match="fusion MLP"):
         ng.Scene(scene)
