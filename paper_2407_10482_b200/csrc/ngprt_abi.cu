@@ -61,11 +61,29 @@ struct ngprt_scene {
     mutable std::mutex prof_mu;
     mutable std::vector<cudaEvent_t> prof_events;
     mutable int prof_launches = 0;
+    // ngprt_render_host context: render + copy streams and device buffers, reused
+    struct HostCtx {
+        std::mutex mu;
+        cudaStream_t render = nullptr, copy = nullptr;
+        float* rgb = nullptr;
+        size_t rgb_cap = 0;
+        ngprt_ray_stats* stats = nullptr;
+        size_t stats_cap = 0;
+        std::vector<cudaEvent_t> band_done;
+    };
+    mutable HostCtx host;
 
     ~ngprt_scene() {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
+        if (host.render) cudaStreamSynchronize(host.render);
+        if (host.copy) cudaStreamSynchronize(host.copy);
+        for (cudaEvent_t e : host.band_done) cudaEventDestroy(e);
+        if (host.render) cudaStreamDestroy(host.render);
+        if (host.copy) cudaStreamDestroy(host.copy);
+        if (host.rgb) cudaFree(host.rgb);
+        if (host.stats) cudaFree(host.stats);
         for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
         cudaSetDevice(prev);
@@ -534,31 +552,101 @@ ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, i
     if (n_cams <= 0) return fail(NGPRT_EINVAL, "ngprt_render_host: n_cams must be > 0");
     NG_CUDA(cudaSetDevice(s->device));
     const bool window = o->w && o->h;
-    const size_t W = window ? o->w : cams[0].width, H = window ? o->h : cams[0].height;
-    const size_t n = W * H * size_t(n_cams);
-    cudaStream_t st;
-    NG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    float* rgb = nullptr;
-    ngprt_ray_stats* stats = nullptr;
+    const uint32_t W = window ? o->w : cams[0].width, H = window ? o->h : cams[0].height;
+    for (int c = 1; c < n_cams; ++c)
+        if (!window && (cams[c].width != W || cams[c].height != H))
+            return fail(NGPRT_EINVAL, "all cameras of one call must share width/height");
+    const size_t per_cam = size_t(W) * H, n = per_cam * size_t(n_cams);
+    // One call at a time per scene through the cached stream pair and buffers.
+    std::lock_guard<std::mutex> lock(s->host.mu);
+    auto& hc = s->host;
+    if (!hc.render) {
+        NG_CUDA(cudaStreamCreateWithFlags(&hc.render, cudaStreamNonBlocking));
+        NG_CUDA(cudaStreamCreateWithFlags(&hc.copy, cudaStreamNonBlocking));
+    }
+    if (hc.rgb_cap < n) {
+        if (hc.rgb) cudaFree(hc.rgb);
+        hc.rgb = nullptr;
+        NG_CUDA(cudaMalloc(&hc.rgb, n * 12));
+        hc.rgb_cap = n;
+    }
+    if (stats_host && hc.stats_cap < n) {
+        if (hc.stats) cudaFree(hc.stats);
+        hc.stats = nullptr;
+        NG_CUDA(cudaMalloc(&hc.stats, n * sizeof(ngprt_ray_stats)));
+        hc.stats_cap = n;
+    }
+    // Pinned (page-locked / registered) host output: the kernels write it directly
+    // over the bus (zero-copy), so the transfer overlaps the deferred-MLP kernel
+    // instead of following it. NGPRT_ZERO_COPY=0 disables.
+    static const bool zc_enabled = [] {
+        const char* e = std::getenv("NGPRT_ZERO_COPY");
+        return !(e && std::atoi(e) == 0);
+    }();
+    auto pinned = [](const void* p) -> void* {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+    };
+    float* rgb_zc = zc_enabled ? static_cast<float*>(pinned(rgb_host)) : nullptr;
+    ngprt_ray_stats* stats_zc =
+        (zc_enabled && stats_host) ? static_cast<ngprt_ray_stats*>(pinned(stats_host)) : nullptr;
+    if (rgb_zc && (!stats_host || stats_zc)) {
+        ngprt_status st = render_impl(s, cams, n_cams, o, rgb_zc, stats_zc, hc.render);
+        const cudaError_t e = cudaStreamSynchronize(hc.render);
+        if (st == NGPRT_OK && e != cudaSuccess)
+            st = fail(NGPRT_ECUDA, std::string("ngprt_render_host: ") + cudaGetErrorString(e));
+        return st;
+    }
+    // Otherwise render to device buffers and copy out; optional row bands let the
+    // copy of band i (copy stream) overlap the render of band i+1. Measured on
+    // B200 the per-band tails cost more than they hide, so one band is the
+    // default; NGPRT_HOST_BANDS overrides.
+    static const int band_override = [] {
+        const char* e = std::getenv("NGPRT_HOST_BANDS");
+        return e ? std::atoi(e) : 0;
+    }();
+    int nb = band_override > 0 ? band_override : 1;
+    nb = std::max(1, std::min<int>(nb, int(H)));
+    while (hc.band_done.size() < size_t(n_cams) * nb) {
+        cudaEvent_t e;
+        NG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        hc.band_done.push_back(e);
+    }
+    const uint32_t x0 = window ? o->x0 : 0, y0 = window ? o->y0 : 0;
     ngprt_status status = NGPRT_OK;
-    if (cudaMallocAsync(&rgb, n * 12, st) != cudaSuccess ||
-        (stats_host && cudaMallocAsync(&stats, n * sizeof(ngprt_ray_stats), st) != cudaSuccess)) {
-        status = fail(NGPRT_ENOMEM, "ngprt_render_host: device allocation failed");
-    } else {
-        status = render_impl(s, cams, n_cams, o, rgb, stats, st);
-        if (status == NGPRT_OK) {
-            cudaMemcpyAsync(rgb_host, rgb, n * 12, cudaMemcpyDeviceToHost, st);
+    for (int c = 0; c < n_cams && status == NGPRT_OK; ++c) {
+        for (int b = 0; b < nb && status == NGPRT_OK; ++b) {
+            const uint32_t r0 = uint32_t(size_t(H) * b / nb), r1 = uint32_t(size_t(H) * (b + 1) / nb);
+            if (r1 <= r0) continue;
+            ngprt_render_opts ob = *o;
+            ob.x0 = x0;
+            ob.y0 = y0 + r0;
+            ob.w = W;
+            ob.h = r1 - r0;
+            const size_t off = size_t(c) * per_cam + size_t(r0) * W;
+            const size_t cnt = size_t(r1 - r0) * W;
+            status = render_impl(s, cams + c, 1, &ob, hc.rgb + 3 * off,
+                                 stats_host ? hc.stats + off : nullptr, hc.render);
+            if (status != NGPRT_OK) break;
+            cudaEvent_t ev = hc.band_done[size_t(c) * nb + b];
+            cudaEventRecord(ev, hc.render);
+            cudaStreamWaitEvent(hc.copy, ev, 0);
+            cudaMemcpyAsync(rgb_host + 3 * off, hc.rgb + 3 * off, cnt * 12, cudaMemcpyDeviceToHost,
+                            hc.copy);
             if (stats_host)
-                cudaMemcpyAsync(stats_host, stats, n * sizeof(ngprt_ray_stats),
-                                cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(stats_host + off, hc.stats + off, cnt * sizeof(ngprt_ray_stats),
+                                cudaMemcpyDeviceToHost, hc.copy);
         }
     }
-    if (rgb) cudaFreeAsync(rgb, st);
-    if (stats) cudaFreeAsync(stats, st);
-    const cudaError_t e = cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
-    if (status == NGPRT_OK && e != cudaSuccess)
-        status = fail(NGPRT_ECUDA, std::string("ngprt_render_host: ") + cudaGetErrorString(e));
+    const cudaError_t e1 = cudaStreamSynchronize(hc.render);
+    const cudaError_t e2 = cudaStreamSynchronize(hc.copy);
+    if (status == NGPRT_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
+        status = fail(NGPRT_ECUDA, std::string("ngprt_render_host: ") +
+                                       cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
     return status;
 }
 
