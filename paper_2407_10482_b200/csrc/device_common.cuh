@@ -133,7 +133,9 @@ struct DevScene {
     int occ_pow2;                                   // every r_k is a power of two
     // Probe code per level-1 voxel (r1^3 u16): bits 8..10 = e, the number of
     // pyramid levels 4..1 whose bit is set before the first clear one (e = 4:
-    // all set, level 0 decides); bits 0..7 = distance value G when dist_res == r1.
+    // all set, level 0 decides); bits 0..7 = the 8 level-0 child bits when
+    // e == 4, else the distance value G (when dist_res == r1). One load answers
+    // occupancy_probe and the distance read of a marching point.
     const uint16_t* probe;
     int dist_is_l1;                                 // dist_res == r1
     float dist_h;                                   // float(dist_res)/2.0f

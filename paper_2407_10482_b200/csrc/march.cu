@@ -475,8 +475,9 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     int exit_k;
     if (e == 4) {
         s.n_occ_acc += 5;
-        const uint32_t bi = uint32_t(i0[0]) + uint32_t(r0) * (uint32_t(i0[1]) + uint32_t(r0) * uint32_t(i0[2]));
-        if ((__ldg(sc.occ[0] + (bi >> 5)) >> (bi & 31u)) & 1u) {
+        // level-0 bit from the code's child byte (no second dependent load)
+        const uint32_t child = uint32_t(i0[0] & 1) | (uint32_t(i0[1] & 1) << 1) | (uint32_t(i0[2] & 1) << 2);
+        if ((code >> child) & 1u) {
             ++s.n_occ;
             s.pending = true;
             return true;
@@ -699,8 +700,24 @@ __global__ void probe_code_kernel(const DevScene sc, uint16_t* __restrict__ out)
             if (!((sc.occ[k][b >> 5] >> (b & 31)) & 1u)) break;
             ++e;
         }
-        const uint32_t g = (sc.dist && sc.dist_is_l1) ? sc.dist[i] : 0u;
-        out[i] = uint16_t((e << 8) | g);
+        // Payload byte: the pyramid is an OR-reduction, so a level-1 voxel with
+        // e == 4 is occupied (its distance value is 0) and one with e < 4 has 8
+        // empty children. The byte therefore carries the 8 level-0 child bits
+        // (bit c = child (c&1, c>>1&1, c>>2)) when e == 4, else the distance value.
+        uint32_t payload;
+        if (e == 4) {
+            payload = 0;
+            const int r0 = sc.occ_res[0];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const size_t b = size_t(2 * x + (c & 1)) +
+                                 size_t(r0) * (size_t(2 * y + ((c >> 1) & 1)) + size_t(r0) * size_t(2 * z + (c >> 2)));
+                payload |= ((sc.occ[0][b >> 5] >> (b & 31)) & 1u) << c;
+            }
+        } else {
+            payload = (sc.dist && sc.dist_is_l1) ? sc.dist[i] : 0u;
+        }
+        out[i] = uint16_t((e << 8) | payload);
     }
 }
 
