@@ -143,6 +143,7 @@ struct DevScene {
     float coarse_h;                                 // float(L_C)/2.0f
     float fine_h[NGPRT_MAX_FINE_LEVELS];            // float(fine_res[l])/2.0f
     int coarse_u32;                                 // (L_C+1)^3 < 2^32: 32-bit corner keys
+    int fast_decode;                                // coarse_u32 and every level pow2-hashed
 };
 
 constexpr int kPsiW0 = 0, kPsiB0 = 64 * 23, kPsiW1 = kPsiB0 + 64, kPsiB1 = kPsiW1 + 64 * 64,

@@ -399,6 +399,152 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
     }
 }
 
+// Fast-path decode (fp16 storage, power-of-two hashed fine levels, 32-bit
+// coarse keys): the coarse rows and the rows of the first P fine levels are
+// requested before any of them is consumed, so a sample costs one dependent
+// gather round trip instead of 1 + L. Arithmetic and its order are exactly
+// decode_point's (same per-corner accumulation, same in-order fuse).
+#ifndef NGPRT_FINE_PREFETCH
+#define NGPRT_FINE_PREFETCH 1
+#endif
+template <int L>
+__device__ __forceinline__ void decode_point_fast(const DevScene& sc, const float x[3],
+                                                  int keep_level, const unsigned long long* tab,
+                                                  float* scr, float out[8]) {
+    constexpr int W = 8 + 2 * L;
+    constexpr int P = NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L;
+    constexpr int CW = W <= 12 ? 6 : 8;  // u32 words of a coarse row actually needed
+    // ---- issue: coarse rows ----
+    int cb[3];
+    float cf[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.coarse_h, sc.L_C, cb[a], cf[a]);
+    const uint32_t r1 = uint32_t(sc.L_C) + 1;
+    const uint32_t key0 = uint32_t(cb[0]) + r1 * (uint32_t(cb[1]) + r1 * uint32_t(cb[2]));
+    uint32_t craw[8][CW];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint4* p = reinterpret_cast<const uint4*>(sc.coarse) +
+                         size_t(key0 + (k & 1) + ((k >> 1) & 1) * r1 + (k >> 2) * r1 * r1) * 2;
+        if constexpr (CW == 8) {
+            uint32_t r[8];
+            ldg256(p, r);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) craw[k][i] = r[i];
+        } else {
+            const uint4 a = __ldg(p);
+            const uint2 b = __ldg(reinterpret_cast<const uint2*>(p + 1));
+            craw[k][0] = a.x; craw[k][1] = a.y; craw[k][2] = a.z; craw[k][3] = a.w;
+            craw[k][4] = b.x; craw[k][5] = b.y;
+        }
+    }
+    // ---- issue: fine levels 0..P-1 ----
+    uint4 fraw[P][8];
+    float ff[P][3];
+#pragma unroll
+    for (int l = 0; l < P; ++l) {
+        int b[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[l], sc.fine_res[l], b[a], ff[l][a]);
+        const uint32_t mask = sc.fine_mask[l];
+        const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
+        const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
+        const uint4* table = reinterpret_cast<const uint4*>(sc.fine[l]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            fraw[l][k] = __ldg(table + ((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask));
+    }
+    // ---- coarse interpolation (baking.hpp:72-78) ----
+    float dec[W];
+    {
+        float w[8];
+        corner_weights(cf, w);
+#pragma unroll
+        for (int i = 0; i < W; ++i) dec[i] = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int i = 0; i < W / 2; ++i) {
+                const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&craw[k][i]));
+                dec[2 * i] += w[k] * v.x;
+                dec[2 * i + 1] += w[k] * v.y;
+            }
+    }
+    // ---- attention (split_decoder_output, model.hpp:18-21) ----
+    const int mode = sc.fusion;
+    const bool variant = mode == NGPRT_FUSION_SEPARATE_ATT_V || mode == NGPRT_FUSION_SHARED_ATT_V;
+    if (variant) {
+#pragma unroll
+        for (int j = 0; j < 2 * L; ++j) scr[j * kBlock] = dec[8 + j];
+        const int jstep = mode == NGPRT_FUSION_SHARED_ATT_V ? 2 : 1;
+#pragma unroll 1
+        for (int j = 0; j < 2 * L; j += 2 * jstep) {
+            const int j2 = j + jstep;
+            const bool two = j2 < 2 * L;
+            const float y0 = activate_sigmoid(scr[j * kBlock], tab);
+            const float y1 = activate_sigmoid(two ? scr[j2 * kBlock] : 0.0f, tab);
+            scr[j * kBlock] = y0;
+            if (two) scr[j2 * kBlock] = y1;
+        }
+    }
+    auto weights = [&](int l, float& wo, float& wb) {
+        if (variant) {
+            wo = scr[2 * l * kBlock];
+            wb = mode == NGPRT_FUSION_SEPARATE_ATT_V ? scr[(2 * l + 1) * kBlock] : wo;
+        } else if (mode == NGPRT_FUSION_SUM) {
+            wo = wb = 1.0f;
+        } else {
+            wo = sc.att_w[2 * l];
+            wb = mode == NGPRT_FUSION_SHARED_ATT_INV ? wo : sc.att_w[2 * l + 1];
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[i] = dec[i];
+    // ---- prefetched fine levels: interpolate (hash_grid.hpp:98-103) and fuse in order ----
+#pragma unroll
+    for (int l = 0; l < P; ++l) {
+        float w[8];
+        corner_weights(ff[l], w);
+        float fine[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) fine[c] = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const __half2* h = reinterpret_cast<const __half2*>(&fraw[l][k]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 v = __half22float2(h[i]);
+                fine[2 * i] += w[k] * v.x;
+                fine[2 * i + 1] += w[k] * v.y;
+            }
+        }
+        if (keep_level > 0 && l + 1 != keep_level) {
+#pragma unroll
+            for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
+        }
+        float wo, wb;
+        weights(l, wo, wb);
+        out[0] += wo * fine[0];
+#pragma unroll
+        for (int c = 1; c < 8; ++c) out[c] += wb * fine[c];
+    }
+    // ---- remaining levels one round trip each ----
+#pragma unroll 1
+    for (int l = P; l < L; ++l) {
+        float fine[8];
+        fine_level<true>(sc, l, x, fine);
+        if (keep_level > 0 && l + 1 != keep_level) {
+#pragma unroll
+            for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
+        }
+        float wo, wb;
+        weights(l, wo, wb);
+        out[0] += wo * fine[0];
+#pragma unroll
+        for (int c = 1; c < 8; ++c) out[c] += wb * fine[c];
+    }
+}
+
 // Per-lane ray state.
 struct Lane {
     Ray ray;
@@ -592,7 +738,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             // ---- decode phase: emit(t) of the canonical render_ray ----
             if (s.has_ray && s.pending) {
                 float f[8];
-                decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
+                if constexpr (F16 && !MLPF) {
+                    if (sc.fast_decode)
+                        decode_point_fast<L>(sc, s.xc, p.keep_level, tab, scr, f);
+                    else
+                        decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
+                } else {
+                    decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
+                }
                 // composite, volume.hpp:61-70
                 const float sigma = activate_density(f[0], tab);
                 const float a = alpha_from_sigma(sigma, step, tab);

@@ -349,6 +349,9 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         ds.coarse_h = float(ds.L_C) / 2.0f;
         for (int l = 0; l < L; ++l) ds.fine_h[l] = float(ds.fine_res[l]) / 2.0f;
         ds.coarse_u32 = n_corner < (uint64_t(1) << 32);
+        ds.fast_decode = ds.coarse_u32;
+        for (int l = 0; l < L; ++l) ds.fast_decode &= ds.fine_mode[l] == 1;
+        if (const char* e = std::getenv("NGPRT_FAST_DECODE")) ds.fast_decode &= std::atoi(e) != 0;
         const size_t r1 = size_t(ds.occ_res[1]);
         uint16_t* probe;
         NG_TRY(s->alloc(&probe, r1 * r1 * r1 * 2));
