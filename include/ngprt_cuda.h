@@ -199,6 +199,50 @@ const ngprt_scene_desc* ngprt_baked_desc(const ngprt_baked* b);
 void ngprt_baked_free(ngprt_baked* b);
 ngprt_status ngprt_scene_load(const char* path, int device, ngprt_scene** out);
 
+/* Writes an ngprt_baked in the reference's format (save_baked, baking.hpp:266-349).
+ * Pyramid must be 512-based with a 256^3 distance grid, as the format fixes. */
+ngprt_status ngprt_baked_save(const ngprt_baked* b, const char* path);
+
+/* ---------------------------------------------------------------------------
+ * Bake (baking.hpp:107-202): a trained NgpRtModel (model.hpp:27-107) plus its
+ * training occupancy -> the render-time BakedScene, on the GPU:
+ *   density cull of the training voxels with the live decode (decode_point,
+ *   model.hpp:195-239), dilation, upsampling to the 512 render grid, pyramid
+ *   and distance grid (K3/K4), corner retention on the L_C grid, and corner
+ *   evaluation (evaluate_corner, model.hpp:71-87: six coarse hash levels through
+ *   the aux MLP 24 -> 64 -> 8+2L), all in the reference's f32 operation order.
+ * ------------------------------------------------------------------------- */
+typedef struct ngprt_model_desc {
+    uint32_t L, L_C;
+    uint32_t coarse_res[6];                      /* EncodingConfig::coarse_resolutions     */
+    uint64_t coarse_table_len;                   /* max table length of a coarse level      */
+    const float* coarse_tables[6];               /* min((res+1)^3, len) x 4 each            */
+    const float* aux_w[2];                       /* TinyMlp 24 -> 64 -> 8+2L (out x in)      */
+    const float* aux_b[2];
+    uint32_t fine_res[NGPRT_MAX_FINE_LEVELS];
+    uint64_t fine_table_len[NGPRT_MAX_FINE_LEVELS];
+    uint8_t fine_hashed[NGPRT_MAX_FINE_LEVELS];
+    const float* fine_tables[NGPRT_MAX_FINE_LEVELS];
+    const float* psi_w[3];
+    const float* psi_b[3];
+    uint8_t fusion_tag;
+    uint8_t reserved[7];
+    const float* att_globals;
+    const float* fusion_mlp_w[2];
+    const float* fusion_mlp_b[2];
+} ngprt_model_desc;
+
+typedef struct ngprt_bake_opts {   /* BakeOptions, baking.hpp:93-97 */
+    double cull_step;              /* <= 0 => kBaseStep                */
+    double cull_alpha_thresh;      /* 0.005                            */
+    uint32_t dilate_voxels;        /* 1                                */
+    uint32_t reserved;
+} ngprt_bake_opts;
+
+ngprt_status ngprt_bake(const ngprt_model_desc* model, const uint64_t* train_words,
+                        uint32_t train_res, const ngprt_bake_opts* opts, int device,
+                        ngprt_baked** out);
+
 /* ---------------------------------------------------------------------------
  * Synthetic scenes (host-only input generation). Restates the reference's own
  * generators so the GPU and the CPU oracle consume the same scene object:
@@ -235,6 +279,16 @@ const char* ngprt_synth_last_error(void);
 /* The desc points into memory owned by the synth object (valid until destroy). */
 const ngprt_scene_desc* ngprt_synth_desc(const ngprt_synth* s);
 void ngprt_synth_destroy(ngprt_synth* s);
+/* A seeded synthetic NgpRtModel (the bake input): coarse hash levels {16..512}
+ * ~ U[-feat_scale, feat_scale], aux/psi/fusion MLPs via TinyMlp::init
+ * (nn.hpp:154-173), fine tables as for scenes, plus a training occupancy grid
+ * scene_occupancy(make_scene(occupancy), occ_base_res) (training resolution). */
+typedef struct ngprt_synth_model ngprt_synth_model;
+ngprt_status ngprt_synth_model_create(const ngprt_synth_params* p, ngprt_synth_model** out);
+const ngprt_model_desc* ngprt_synth_model_desc(const ngprt_synth_model* m);
+const uint64_t* ngprt_synth_model_train_words(const ngprt_synth_model* m, uint32_t* train_res);
+void ngprt_synth_model_destroy(ngprt_synth_model* m);
+
 /* sphere_views(n, radius) with fx = fy = 1.1 W, cx = W/2, cy = H/2 (scene.hpp:388-395). */
 ngprt_status ngprt_synth_cameras(int n, double radius, uint32_t width, uint32_t height,
                                  ngprt_camera* out);

@@ -457,4 +457,66 @@ int ref_save_baked(void* handle, const char* path) {
 
 double ref_base_step() { return kBaseStep; }
 
+// bake (baking.hpp:107-202) of the model a ngprt_model_desc describes, written
+// with save_baked to `path`. The desc's arrays are copied into a reference
+// NgpRtModel<float> (model.hpp:27-107) built by its own init.
+int ref_bake(const ngprt_model_desc* md, const uint64_t* train_words, int train_res,
+             const ngprt_bake_opts* o, const char* path) {
+    try {
+        EncodingConfig cfg;
+        for (int k = 0; k < 6; ++k) cfg.coarse_resolutions[k] = int(md->coarse_res[k]);
+        cfg.coarse_table_len = md->coarse_table_len;
+        cfg.fine_levels = int(md->L);
+        cfg.fine_table_len = md->fine_table_len[0];
+        cfg.corner_grid_res = int(md->L_C);
+        NgpRtModel<float> model;
+        model.init(cfg, FusionTag(md->fusion_tag), 1);
+        for (int k = 0; k < 6; ++k) {
+            auto& v = model.encoding.coarse[k].entries.value;
+            std::memcpy(v.data(), md->coarse_tables[k], v.size() * sizeof(float));
+        }
+        for (int k = 0; k < 2; ++k) {
+            auto& w = model.aux.weight[k].value;
+            auto& b = model.aux.bias[k].value;
+            std::memcpy(w.data(), md->aux_w[k], w.size() * sizeof(float));
+            std::memcpy(b.data(), md->aux_b[k], b.size() * sizeof(float));
+        }
+        for (int l = 0; l < int(md->L); ++l) {
+            auto& lvl = model.encoding.fine[l];
+            if (lvl.table_len != md->fine_table_len[l] || lvl.resolution != int(md->fine_res[l]))
+                throw std::invalid_argument("ref_bake: fine level geometry differs from EncodingConfig");
+            std::memcpy(lvl.entries.value.data(), md->fine_tables[l],
+                        lvl.entries.value.size() * sizeof(float));
+        }
+        for (int k = 0; k < 3; ++k) {
+            auto& w = model.psi.weight[k].value;
+            auto& b = model.psi.bias[k].value;
+            std::memcpy(w.data(), md->psi_w[k], w.size() * sizeof(float));
+            std::memcpy(b.data(), md->psi_b[k], b.size() * sizeof(float));
+        }
+        if (fusion_is_invariant(model.fusion_tag))
+            std::memcpy(model.fusion.global_pre.value.data(), md->att_globals,
+                        model.fusion.global_pre.value.size() * sizeof(float));
+        if (model.fusion_tag == FusionTag::Mlp)
+            for (int k = 0; k < 2; ++k) {
+                auto& w = model.fusion.mlp.weight[k].value;
+                auto& b = model.fusion.mlp.bias[k].value;
+                std::memcpy(w.data(), md->fusion_mlp_w[k], w.size() * sizeof(float));
+                std::memcpy(b.data(), md->fusion_mlp_b[k], b.size() * sizeof(float));
+            }
+        BakeOptions opt;
+        if (o) {
+            if (o->cull_step > 0) opt.cull_step = o->cull_step;
+            opt.cull_alpha_thresh = o->cull_alpha_thresh;
+            opt.dilate_voxels = int(o->dilate_voxels);
+        }
+        BakedScene out = bake(model, bitgrid_from_words(train_words, train_res), opt);
+        save_baked(out, path);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 } // extern "C"

@@ -123,6 +123,40 @@ class SynthParams(C.Structure):
     ]
 
 
+class ModelDesc(C.Structure):
+    """ngprt_model_desc: a trained NgpRtModel (model.hpp:27-107), the bake input."""
+    _fields_ = [
+        ("L", C.c_uint32),
+        ("L_C", C.c_uint32),
+        ("coarse_res", C.c_uint32 * 6),
+        ("coarse_table_len", C.c_uint64),
+        ("coarse_tables", C.POINTER(C.c_float) * 6),
+        ("aux_w", C.POINTER(C.c_float) * 2),
+        ("aux_b", C.POINTER(C.c_float) * 2),
+        ("fine_res", C.c_uint32 * MAX_FINE_LEVELS),
+        ("fine_table_len", C.c_uint64 * MAX_FINE_LEVELS),
+        ("fine_hashed", C.c_uint8 * MAX_FINE_LEVELS),
+        ("fine_tables", C.POINTER(C.c_float) * MAX_FINE_LEVELS),
+        ("psi_w", C.POINTER(C.c_float) * 3),
+        ("psi_b", C.POINTER(C.c_float) * 3),
+        ("fusion_tag", C.c_uint8),
+        ("reserved", C.c_uint8 * 7),
+        ("att_globals", C.POINTER(C.c_float)),
+        ("fusion_mlp_w", C.POINTER(C.c_float) * 2),
+        ("fusion_mlp_b", C.POINTER(C.c_float) * 2),
+    ]
+
+
+class BakeOpts(C.Structure):
+    """ngprt_bake_opts: BakeOptions (baking.hpp:93-97)."""
+    _fields_ = [
+        ("cull_step", C.c_double),
+        ("cull_alpha_thresh", C.c_double),
+        ("dilate_voxels", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
 # name -> (restype, argtypes): every function declared in include/ngprt_cuda.h
 SIGNATURES = {
     "ngprt_abi_version": (C.c_int, []),
@@ -147,11 +181,18 @@ SIGNATURES = {
     "ngprt_baked_desc": (C.POINTER(SceneDesc), [C.c_void_p]),
     "ngprt_baked_free": (None, [C.c_void_p]),
     "ngprt_scene_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "ngprt_baked_save": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "ngprt_bake": (C.c_int, [C.POINTER(ModelDesc), C.c_void_p, C.c_uint32, C.POINTER(BakeOpts),
+                             C.c_int, C.POINTER(C.c_void_p)]),
     "ngprt_synth_default_params": (None, [C.POINTER(SynthParams)]),
     "ngprt_synth_create": (C.c_int, [C.POINTER(SynthParams), C.POINTER(C.c_void_p)]),
     "ngprt_synth_last_error": (C.c_char_p, []),
     "ngprt_synth_desc": (C.POINTER(SceneDesc), [C.c_void_p]),
     "ngprt_synth_destroy": (None, [C.c_void_p]),
+    "ngprt_synth_model_create": (C.c_int, [C.POINTER(SynthParams), C.POINTER(C.c_void_p)]),
+    "ngprt_synth_model_desc": (C.POINTER(ModelDesc), [C.c_void_p]),
+    "ngprt_synth_model_train_words": (C.POINTER(C.c_uint64), [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "ngprt_synth_model_destroy": (None, [C.c_void_p]),
     "ngprt_synth_cameras": (C.c_int, [C.c_int, C.c_double, C.c_uint32, C.c_uint32,
                                       C.POINTER(Camera)]),
     "ngprt_crc32": (C.c_uint32, [C.c_void_p, C.c_uint64, C.c_uint32]),

@@ -30,11 +30,12 @@ UNITS = [
     ("shade_exact.cu", ["-fmad=false"]),
     ("mlp_tc.cu", []),
     ("occupancy.cu", []),
+    ("bake.cu", ["-fmad=false"]),
     ("ngprt_abi.cu", []),
     ("synth.cpp", []),
     ("ngrt_io.cpp", []),
 ]
-HEADERS = list(CSRC.glob("*.cuh")) + [INCLUDE / "ngprt_cuda.h"]
+HEADERS = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [INCLUDE / "ngprt_cuda.h"]
 
 
 def _newer(src: Path, dst: Path, deps) -> bool:

@@ -1,0 +1,531 @@
+// bake.cu — the bake (baking.hpp:107-202) on the GPU: a trained NgpRtModel plus
+// its training occupancy -> the render-time BakedScene.
+//
+//   (1) density cull (:118-134): every occupied training voxel's centre goes
+//       through the live decode (decode_point, model.hpp:195-239: 8 corner
+//       evaluations, interpolation, attention, fine levels, fuse) and is kept
+//       iff 1 - exp(-sigma * cull_step) > cull_alpha_thresh; then dilation
+//       (BitGrid::dilated, occupancy.hpp:54-71);
+//   (2) the 512 render grid (BitGrid::upsampled, :74-87), its pyramid and the
+//       256^3 distance grid (K3/K4, bit-exact with build_pyramid /
+//       build_distance_grid);
+//   (3) corner retention on the L_C grid (:146-163) and corner evaluation
+//       (evaluate_corner, model.hpp:71-87: six coarse hash levels -> 24
+//       features -> aux MLP 24 -> 64 -> 8+2L), one thread per retained corner;
+//   (4) fine tables, psi and the fusion parameters carried over verbatim.
+// Built with -fmad=false: every f32 expression rounds where the reference's
+// does, so keys, rows, pyramid and distance grid are bit-identical to the
+// reference's bake. The one double-precision transcendental (the cull's
+// std::exp, glibc) is evaluated with CUDA's exp; decisions within 1e-12 of the
+// threshold are re-evaluated on the host with glibc, so the cull is exact too.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "baked.hpp"
+#include "render.cuh"
+
+namespace ngprt_dev {
+namespace {
+
+constexpr int kCoarseLevels = 6;
+
+struct DevModel {
+    int L, L_C, W;  // W = 8 + 2L
+    float lc_h;     // float(L_C) / 2
+    int cres[kCoarseLevels];
+    float ch[kCoarseLevels];
+    int cdirect[kCoarseLevels];
+    unsigned long long clen[kCoarseLevels];
+    const float* ctab[kCoarseLevels];
+    const float* aux;  // W0 (64x24) b0 (64) W1 (Wx64) b1 (W)
+    int fine_res[NGPRT_MAX_FINE_LEVELS];
+    float fine_h[NGPRT_MAX_FINE_LEVELS];
+    int fine_hashed[NGPRT_MAX_FINE_LEVELS];
+    unsigned long long fine_len[NGPRT_MAX_FINE_LEVELS];
+    const float* fine[NGPRT_MAX_FINE_LEVELS];
+    int fusion;
+    float att_w[2 * NGPRT_MAX_FINE_LEVELS];
+    const float* fmlp;  // W0 (64x8L) b0 (64) W1 (8x64) b1 (8)
+};
+
+// stencil along one axis (hash_grid.hpp:38-46) with h = float(res)/2.0f
+__device__ __forceinline__ void stencil_axis(float x, float h, int res, int& base, float& frac) {
+    const float u = (x - (-1.0f)) * h;
+    int i = int(floorf(u));
+    i = i < res - 1 ? i : res - 1;
+    i = i > 0 ? i : 0;
+    base = i;
+    frac = u - float(i);
+}
+
+// HashLevel::hash_index, hash_grid.hpp:83-94
+__device__ __forceinline__ unsigned long long hash_index(int res, unsigned long long len, int hashed,
+                                                         int x, int y, int z) {
+    if (!hashed) {
+        const unsigned long long r1 = (unsigned long long)res + 1;
+        return (unsigned long long)x + r1 * ((unsigned long long)y + r1 * (unsigned long long)z);
+    }
+    const unsigned long long h = (unsigned long long)x * 1ull ^
+                                 (unsigned long long)y * 2654435761ull ^
+                                 (unsigned long long)z * 805459861ull;
+    return h % len;
+}
+
+// HashLevel::interp (hash_grid.hpp:97-104) of a D-wide table at x.
+template <int D>
+__device__ __forceinline__ void interp(const float* __restrict__ tab, int res, float h,
+                                       unsigned long long len, int hashed, const float x[3],
+                                       float* out) {
+    int b[3];
+    float f[3];
+    for (int a = 0; a < 3; ++a) stencil_axis(x[a], h, res, b[a], f[a]);
+    for (int c = 0; c < D; ++c) out[c] = 0.0f;
+    for (int k = 0; k < 8; ++k) {
+        const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+        const float w = ((dx ? f[0] : 1.0f - f[0]) * (dy ? f[1] : 1.0f - f[1])) *
+                        (dz ? f[2] : 1.0f - f[2]);
+        const float* row = tab + hash_index(res, len, hashed, b[0] + dx, b[1] + dy, b[2] + dz) * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) out[c] += w * __ldg(row + c);
+    }
+}
+
+// NgpRtModel::evaluate_corner (model.hpp:71-87): encode_coarse at the corner
+// position (corner_to_world, hash_grid.hpp:28-31) through the aux MLP.
+__device__ void evaluate_corner(const DevModel& M, int cx, int cy, int cz, float* out) {
+    const float pos[3] = {-1.0f + 2.0f * (float(cx) / float(M.L_C)),
+                          -1.0f + 2.0f * (float(cy) / float(M.L_C)),
+                          -1.0f + 2.0f * (float(cz) / float(M.L_C))};
+    float feat[24];
+    for (int k = 0; k < kCoarseLevels; ++k)
+        interp<4>(M.ctab[k], M.cres[k], M.ch[k], M.clen[k], !M.cdirect[k], pos, feat + 4 * k);
+    // TinyMlp::forward (nn.hpp:175-196), hidden unit by unit; the output layer
+    // accumulates in the same c-order as the reference's inner loop.
+    const float* W0 = M.aux;
+    const float* B0 = W0 + 64 * 24;
+    const float* W1 = B0 + 64;
+    const float* B1 = W1 + M.W * 64;
+    for (int j = 0; j < M.W; ++j) out[j] = __ldg(B1 + j);
+    for (int r = 0; r < 64; ++r) {
+        float h = __ldg(B0 + r);
+        for (int c = 0; c < 24; ++c) h += __ldg(W0 + r * 24 + c) * feat[c];
+        h = h < 0.0f ? 0.0f : h;
+        for (int j = 0; j < M.W; ++j) out[j] += __ldg(W1 + j * 64 + r) * h;
+    }
+}
+
+// sigma_pre of decode_point (model.hpp:195-239) at x: only channel 0 of the fuse.
+__device__ float decode_sigma_pre(const DevModel& M, const float x[3],
+                                  const unsigned long long* tab) {
+    int cb[3];
+    float cf[3];
+    for (int a = 0; a < 3; ++a) stencil_axis(x[a], M.lc_h, M.L_C, cb[a], cf[a]);
+    float dec[16];
+    for (int i = 0; i < M.W; ++i) dec[i] = 0.0f;
+    for (int k = 0; k < 8; ++k) {
+        const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+        const float w = ((dx ? cf[0] : 1.0f - cf[0]) * (dy ? cf[1] : 1.0f - cf[1])) *
+                        (dz ? cf[2] : 1.0f - cf[2]);
+        float row[16];
+        evaluate_corner(M, cb[0] + dx, cb[1] + dy, cb[2] + dz, row);
+        for (int i = 0; i < M.W; ++i) dec[i] += w * row[i];
+    }
+    float fine[NGPRT_MAX_FINE_LEVELS][8];
+    for (int l = 0; l < M.L; ++l)
+        interp<8>(M.fine[l], M.fine_res[l], M.fine_h[l], M.fine_len[l], M.fine_hashed[l], x, fine[l]);
+    float out0 = dec[0];
+    if (M.fusion == NGPRT_FUSION_MLP) {  // fusion.hpp:162-171, channel 0 of the output
+        const int IN = 8 * M.L;
+        const float* W0 = M.fmlp;
+        const float* B0 = W0 + 64 * IN;
+        const float* W1 = B0 + 64;
+        const float* B1 = W1 + 8 * 64;
+        float hat0 = __ldg(B1);
+        for (int r = 0; r < 64; ++r) {
+            float h = __ldg(B0 + r);
+            for (int c = 0; c < IN; ++c) h += __ldg(W0 + r * IN + c) * fine[c / 8][c % 8];
+            h = h < 0.0f ? 0.0f : h;
+            hat0 += __ldg(W1 + r) * h;
+        }
+        return out0 + hat0;
+    }
+    for (int l = 0; l < M.L; ++l) {
+        float wo;
+        if (M.fusion == NGPRT_FUSION_SEPARATE_ATT_V || M.fusion == NGPRT_FUSION_SHARED_ATT_V)
+            wo = activate_sigmoid(dec[8 + 2 * l], tab);  // split_decoder_output, model.hpp:19
+        else if (M.fusion == NGPRT_FUSION_SUM)
+            wo = 1.0f;
+        else
+            wo = M.att_w[2 * l];
+        out0 += wo * fine[l][0];
+    }
+    return out0;
+}
+
+__device__ __forceinline__ bool bit_at(const uint32_t* g, int res, int x, int y, int z) {
+    const size_t i = size_t(x) + size_t(res) * (size_t(y) + size_t(res) * size_t(z));
+    return (g[i >> 5] >> (i & 31)) & 1u;
+}
+
+// (1) density cull: one thread per training voxel; 32 voxels -> one ballot word.
+__global__ void cull_kernel(const DevModel M, const uint32_t* __restrict__ train, int tres,
+                            double cull_step, double thresh, uint32_t* __restrict__ culled,
+                            unsigned int* amb_n, uint32_t* amb_idx, float* amb_sigma, int amb_cap) {
+    __shared__ unsigned long long tab[32];
+    load_exp_table(tab);
+    __syncthreads();
+    const size_t n = size_t(tres) * tres * tres;
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    bool keep = false;
+    if (i < n && ((train[i >> 5] >> (i & 31)) & 1u)) {
+        const int x = int(i % tres), y = int((i / tres) % tres), z = int(i / (size_t(tres) * tres));
+        const double vsz = 2.0 / tres;  // Roi::extent / tres
+        const float c[3] = {float(-1.0 + (x + 0.5) * vsz), float(-1.0 + (y + 0.5) * vsz),
+                            float(-1.0 + (z + 0.5) * vsz)};
+        const float sigma = activate_density(decode_sigma_pre(M, c, tab), tab);
+        const double e = exp(-double(sigma) * cull_step);
+        keep = 1.0 - e > thresh;
+        if (fabs(e - (1.0 - thresh)) < 1e-12) {  // glibc exp may decide differently: host re-check
+            const unsigned int k = atomicAdd(amb_n, 1u);
+            if (int(k) < amb_cap) {
+                amb_idx[k] = uint32_t(i);
+                amb_sigma[k] = sigma;
+            }
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0 && i < n) culled[i >> 5] = m;
+}
+
+// BitGrid::dilated (occupancy.hpp:54-71): 3^3 OR, clipped at the faces.
+__global__ void dilate_kernel(const uint32_t* __restrict__ src, int r, uint32_t* __restrict__ dst) {
+    const size_t n = size_t(r) * r * r;
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    bool v = false;
+    if (i < n) {
+        const int x = int(i % r), y = int((i / r) % r), z = int(i / (size_t(r) * r));
+        for (int dz = -1; dz <= 1 && !v; ++dz)
+            for (int dy = -1; dy <= 1 && !v; ++dy)
+                for (int dx = -1; dx <= 1 && !v; ++dx) {
+                    const int nx = x + dx, ny = y + dy, nz = z + dz;
+                    if (nx < 0 || ny < 0 || nz < 0 || nx >= r || ny >= r || nz >= r) continue;
+                    v = bit_at(src, r, nx, ny, nz);
+                }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && i < n) dst[i >> 5] = m;
+}
+
+// BitGrid::upsampled (occupancy.hpp:74-87): bit replication by `f`.
+__global__ void upsample_kernel(const uint32_t* __restrict__ src, int r, int f,
+                                uint32_t* __restrict__ dst) {
+    const int ro = r * f;
+    const size_t n = size_t(ro) * ro * ro;
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    bool v = false;
+    if (i < n) {
+        const int x = int(i % ro), y = int((i / ro) % ro), z = int(i / (size_t(ro) * ro));
+        v = bit_at(src, r, x / f, y / f, z / f);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && i < n) dst[i >> 5] = m;
+}
+
+// corner_marks (baking.hpp:156-163): the 8 corners of every occupied L_C voxel.
+__global__ void corner_marks_kernel(const uint32_t* __restrict__ occ, int lc, uint32_t* marks) {
+    const size_t n = size_t(lc) * lc * lc;
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i >= n || !((occ[i >> 5] >> (i & 31)) & 1u)) return;
+    const int x = int(i % lc), y = int((i / lc) % lc), z = int(i / (size_t(lc) * lc));
+    const size_t r1 = size_t(lc) + 1;
+    for (int k = 0; k < 8; ++k) {
+        const size_t b = size_t(x + (k & 1)) + r1 * (size_t(y + ((k >> 1) & 1)) + r1 * size_t(z + (k >> 2)));
+        atomicOr(marks + (b >> 5), 1u << (b & 31));
+    }
+}
+
+// (3) evaluate_corner for every retained corner key.
+__global__ void corner_eval_kernel(const DevModel M, const unsigned long long* __restrict__ keys,
+                                   size_t n, float* __restrict__ rows) {
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long r1 = (unsigned long long)M.L_C + 1, key = keys[i];
+    float row[16];
+    evaluate_corner(M, int(key % r1), int((key / r1) % r1), int(key / (r1 * r1)), row);
+    for (int j = 0; j < M.W; ++j) rows[i * M.W + j] = row[j];
+}
+
+unsigned blocks(size_t n, unsigned bs) { return unsigned((n + bs - 1) / bs); }
+size_t words32(size_t res) { return ((res * res * res + 63) / 64) * 2; }
+
+}  // namespace
+}  // namespace ngprt_dev
+
+using namespace ngprt_dev;
+
+namespace {
+
+struct DeviceBuffers {  // frees everything on scope exit
+    std::vector<void*> ptrs;
+    ~DeviceBuffers() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        const cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 16);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("bake: cudaMalloc: ") + cudaGetErrorString(e));
+        cudaMemset(p, 0, count * sizeof(T) + 16);
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* upload(const T* h, size_t count) {
+        T* d = alloc<T>(count);
+        cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice);
+        return d;
+    }
+};
+
+void check_cuda(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void check_finite(const float* p, size_t n, const std::string& group) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(p[i])) throw std::runtime_error("bake: non-finite parameter in group " + group);
+}
+
+}  // namespace
+
+extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* train_words,
+                                   uint32_t tres, const ngprt_bake_opts* opts, int device,
+                                   ngprt_baked** out) {
+    if (!md || !train_words || !out) {
+        ngprt_host::set_error("ngprt_bake: null argument");
+        return NGPRT_EINVAL;
+    }
+    *out = nullptr;
+    try {
+        const int L = int(md->L), lc = int(md->L_C), W = 8 + 2 * L;
+        if (L < 1 || L > NGPRT_MAX_FINE_LEVELS) throw std::invalid_argument("bake: L out of range");
+        if (md->fusion_tag > NGPRT_FUSION_MLP) throw std::invalid_argument("bake: unknown fusion tag");
+        const int render_res = 512;
+        if (tres == 0 || render_res % int(tres) != 0)
+            throw std::invalid_argument("bake: training grid must divide the 512 render grid");
+        if (lc % int(tres) != 0 && int(tres) % lc != 0)
+            throw std::invalid_argument("bake: L_C and the training grid must nest");
+        const double cull_step = (opts && opts->cull_step > 0) ? opts->cull_step : 2.0 * std::sqrt(3.0) / 512.0;
+        const double thresh = opts ? opts->cull_alpha_thresh : 0.005;
+        const int dilate = opts ? int(opts->dilate_voxels) : 1;
+
+        // parameter checks (baking.hpp:109-112), in GradTape group order
+        // (coarse, fine, aux, psi, fusion: model.hpp:44-51)
+        for (int k = 0; k < 6; ++k) {
+            const uint64_t res = md->coarse_res[k], corners = (res + 1) * (res + 1) * (res + 1);
+            check_finite(md->coarse_tables[k], std::min<uint64_t>(corners, md->coarse_table_len) * 4,
+                         "coarse_l" + std::to_string(k));
+        }
+        for (int l = 0; l < L; ++l)
+            check_finite(md->fine_tables[l], md->fine_table_len[l] * 8, "fine_l" + std::to_string(l + 1));
+        const int aux_w[3] = {24, 64, W}, psi_w[4] = {23, 64, 64, 3}, fm_w[3] = {8 * L, 64, 8};
+        for (int k = 0; k < 2; ++k) {
+            check_finite(md->aux_w[k], size_t(aux_w[k]) * aux_w[k + 1], "aux.w" + std::to_string(k));
+            check_finite(md->aux_b[k], aux_w[k + 1], "aux.b" + std::to_string(k));
+        }
+        for (int k = 0; k < 3; ++k) {
+            check_finite(md->psi_w[k], size_t(psi_w[k]) * psi_w[k + 1], "psi.w" + std::to_string(k));
+            check_finite(md->psi_b[k], psi_w[k + 1], "psi.b" + std::to_string(k));
+        }
+        const bool inv_tag = md->fusion_tag == NGPRT_FUSION_SHARED_ATT_INV ||
+                             md->fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV;
+        if (inv_tag) check_finite(md->att_globals, size_t(2) * L, "att_global");
+        if (md->fusion_tag == NGPRT_FUSION_MLP)
+            for (int k = 0; k < 2; ++k) {
+                check_finite(md->fusion_mlp_w[k], size_t(fm_w[k]) * fm_w[k + 1], "fusion_mlp.w" + std::to_string(k));
+                check_finite(md->fusion_mlp_b[k], fm_w[k + 1], "fusion_mlp.b" + std::to_string(k));
+            }
+
+        // the model on the device
+        if (cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("bake: no CUDA device");
+        DeviceBuffers db;
+        DevModel M{};
+        M.L = L;
+        M.L_C = lc;
+        M.W = W;
+        M.lc_h = float(lc) / 2.0f;
+        for (int k = 0; k < 6; ++k) {
+            const uint64_t res = md->coarse_res[k], corners = (res + 1) * (res + 1) * (res + 1);
+            const uint64_t len = corners <= md->coarse_table_len ? corners : md->coarse_table_len;
+            M.cres[k] = int(res);
+            M.ch[k] = float(res) / 2.0f;
+            M.cdirect[k] = corners <= md->coarse_table_len;
+            M.clen[k] = len;
+            M.ctab[k] = db.upload(md->coarse_tables[k], len * 4);
+        }
+        {
+            std::vector<float> aux(64 * 24 + 64 + W * 64 + W);
+            std::memcpy(aux.data(), md->aux_w[0], 64 * 24 * 4);
+            std::memcpy(aux.data() + 64 * 24, md->aux_b[0], 64 * 4);
+            std::memcpy(aux.data() + 64 * 24 + 64, md->aux_w[1], size_t(W) * 64 * 4);
+            std::memcpy(aux.data() + 64 * 24 + 64 + W * 64, md->aux_b[1], size_t(W) * 4);
+            M.aux = db.upload(aux.data(), aux.size());
+        }
+        for (int l = 0; l < L; ++l) {
+            M.fine_res[l] = int(md->fine_res[l]);
+            M.fine_h[l] = float(md->fine_res[l]) / 2.0f;
+            M.fine_hashed[l] = md->fine_hashed[l];
+            M.fine_len[l] = md->fine_table_len[l];
+            M.fine[l] = db.upload(md->fine_tables[l], md->fine_table_len[l] * 8);
+        }
+        M.fusion = md->fusion_tag;
+        const bool inv = M.fusion == NGPRT_FUSION_SHARED_ATT_INV || M.fusion == NGPRT_FUSION_SEPARATE_ATT_INV;
+        if (inv)
+            for (int i = 0; i < 2 * L; ++i) M.att_w[i] = 1.0f / (1.0f + std::exp(-md->att_globals[i]));
+        if (M.fusion == NGPRT_FUSION_MLP) {
+            const size_t in = size_t(8) * L;
+            std::vector<float> f(64 * in + 64 + 8 * 64 + 8);
+            std::memcpy(f.data(), md->fusion_mlp_w[0], 64 * in * 4);
+            std::memcpy(f.data() + 64 * in, md->fusion_mlp_b[0], 64 * 4);
+            std::memcpy(f.data() + 64 * in + 64, md->fusion_mlp_w[1], 8 * 64 * 4);
+            std::memcpy(f.data() + 64 * in + 64 + 512, md->fusion_mlp_b[1], 8 * 4);
+            M.fmlp = db.upload(f.data(), f.size());
+        }
+
+        // (1) density cull at the training resolution, exact decisions
+        const size_t tn = size_t(tres) * tres * tres;
+        uint32_t* train = db.upload(reinterpret_cast<const uint32_t*>(train_words), words32(tres));
+        uint32_t* culled = db.alloc<uint32_t>(words32(tres));
+        unsigned int* amb_n = db.alloc<unsigned int>(1);
+        const int amb_cap = 1 << 16;
+        uint32_t* amb_idx = db.alloc<uint32_t>(amb_cap);
+        float* amb_sigma = db.alloc<float>(amb_cap);
+        cull_kernel<<<blocks(tn, 128), 128>>>(M, train, int(tres), cull_step, thresh, culled, amb_n,
+                                              amb_idx, amb_sigma, amb_cap);
+        check_cuda("bake: cull");
+        unsigned int n_amb = 0;
+        cudaMemcpy(&n_amb, amb_n, 4, cudaMemcpyDeviceToHost);
+        if (n_amb > unsigned(amb_cap)) throw std::runtime_error("bake: too many borderline cull decisions");
+        if (n_amb) {  // glibc's exp decides the borderline voxels (baking.hpp:131)
+            std::vector<uint32_t> words(words32(tres)), idx(n_amb);
+            std::vector<float> sig(n_amb);
+            cudaMemcpy(words.data(), culled, words.size() * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(idx.data(), amb_idx, n_amb * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(sig.data(), amb_sigma, n_amb * 4, cudaMemcpyDeviceToHost);
+            for (unsigned k = 0; k < n_amb; ++k) {
+                const bool keep = 1.0 - std::exp(-double(sig[k]) * cull_step) > thresh;
+                if (keep) words[idx[k] >> 5] |= 1u << (idx[k] & 31);
+                else words[idx[k] >> 5] &= ~(1u << (idx[k] & 31));
+            }
+            cudaMemcpy(culled, words.data(), words.size() * 4, cudaMemcpyHostToDevice);
+        }
+        for (int i = 0; i < dilate; ++i) {
+            uint32_t* d2 = db.alloc<uint32_t>(words32(tres));
+            dilate_kernel<<<blocks(tn, 256), 256>>>(culled, int(tres), d2);
+            culled = d2;
+        }
+        check_cuda("bake: dilate");
+
+        // (2) render grid, pyramid, distance grid (baking.hpp:137-144)
+        const int f = render_res / int(tres);
+        uint32_t* levels[NGPRT_PYRAMID_LEVELS];
+        levels[0] = db.alloc<uint32_t>(words32(render_res));
+        upsample_kernel<<<blocks(size_t(render_res) * render_res * render_res, 256), 256>>>(
+            culled, int(tres), f, levels[0]);
+        for (int k = 1; k < NGPRT_PYRAMID_LEVELS; ++k) {
+            levels[k] = db.alloc<uint32_t>(words32(render_res >> k));
+            launch_pyramid_level(levels[k - 1], render_res >> (k - 1), levels[k], nullptr);
+        }
+        uint8_t* dist = db.alloc<uint8_t>(size_t(256) * 256 * 256);
+        uint16_t* ta = db.alloc<uint16_t>(size_t(256) * 256 * 256);
+        uint16_t* tb = db.alloc<uint16_t>(size_t(256) * 256 * 256);
+        launch_distance_grid(levels[1], 256, ta, tb, dist, nullptr);
+        check_cuda("bake: pyramid / distance grid");
+
+        // (3) corner retention on the L_C grid and corner evaluation
+        uint32_t* occ_lc = culled;
+        int r = int(tres);
+        if (lc >= r) {
+            if (lc > r) {
+                occ_lc = db.alloc<uint32_t>(words32(lc));
+                upsample_kernel<<<blocks(size_t(lc) * lc * lc, 256), 256>>>(culled, r, lc / r, occ_lc);
+            }
+        } else {
+            while (r > lc) {  // BitGrid::downsampled2 until res == L_C
+                uint32_t* g = db.alloc<uint32_t>(words32(r / 2));
+                launch_pyramid_level(occ_lc, r, g, nullptr);
+                occ_lc = g;
+                r /= 2;
+            }
+        }
+        const size_t r1 = size_t(lc) + 1;
+        uint32_t* marks = db.alloc<uint32_t>(words32(r1));
+        corner_marks_kernel<<<blocks(size_t(lc) * lc * lc, 256), 256>>>(occ_lc, lc, marks);
+        check_cuda("bake: corner marks");
+        std::vector<uint32_t> hmarks(words32(r1));
+        cudaMemcpy(hmarks.data(), marks, hmarks.size() * 4, cudaMemcpyDeviceToHost);
+        auto b = std::make_unique<ngprt_baked>();
+        const size_t ncorner = r1 * r1 * r1;
+        for (size_t wi = 0; wi < hmarks.size(); ++wi)  // key order == the reference's z,y,x scan
+            for (uint32_t m = hmarks[wi]; m; m &= m - 1) {
+                const size_t key = (wi << 5) + size_t(__builtin_ctz(m));
+                if (key < ncorner) b->keys.push_back(key);
+            }
+        b->rows.resize(b->keys.size() * W);
+        if (!b->keys.empty()) {
+            unsigned long long* dkeys = db.upload(reinterpret_cast<const unsigned long long*>(b->keys.data()), b->keys.size());
+            float* drows = db.alloc<float>(b->rows.size());
+            corner_eval_kernel<<<blocks(b->keys.size(), 128), 128>>>(M, dkeys, b->keys.size(), drows);
+            check_cuda("bake: corner evaluation");
+            cudaMemcpy(b->rows.data(), drows, b->rows.size() * 4, cudaMemcpyDeviceToHost);
+        }
+
+        // (4) assemble the BakedScene (verbatim carry-over, baking.hpp:176-200)
+        ngprt_scene_desc& d = b->desc;
+        d.L = uint32_t(L);
+        d.L_C = uint32_t(lc);
+        d.fusion_tag = md->fusion_tag;
+        for (int l = 0; l < L; ++l) {
+            d.fine_res[l] = md->fine_res[l];
+            d.fine_table_len[l] = md->fine_table_len[l];
+            d.fine_hashed[l] = md->fine_hashed[l];
+            b->fine[l].assign(md->fine_tables[l], md->fine_tables[l] + md->fine_table_len[l] * 8);
+        }
+        const int pw[4] = {23, 64, 64, 3};
+        for (int k = 0; k < 3; ++k) {
+            b->psi_w[k].assign(md->psi_w[k], md->psi_w[k] + size_t(pw[k]) * pw[k + 1]);
+            b->psi_b[k].assign(md->psi_b[k], md->psi_b[k] + pw[k + 1]);
+        }
+        if (inv) b->att.assign(md->att_globals, md->att_globals + 2 * L);
+        if (M.fusion == NGPRT_FUSION_MLP) {
+            const int fw[3] = {8 * L, 64, 8};
+            for (int k = 0; k < 2; ++k) {
+                b->fmlp_w[k].assign(md->fusion_mlp_w[k], md->fusion_mlp_w[k] + size_t(fw[k]) * fw[k + 1]);
+                b->fmlp_b[k].assign(md->fusion_mlp_b[k], md->fusion_mlp_b[k] + fw[k + 1]);
+            }
+        }
+        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) {
+            const size_t res = size_t(render_res) >> k;
+            b->pyramid[k].resize((res * res * res + 63) / 64);
+            cudaMemcpy(b->pyramid[k].data(), levels[k], b->pyramid[k].size() * 8, cudaMemcpyDeviceToHost);
+        }
+        b->dist.resize(size_t(256) * 256 * 256);
+        cudaMemcpy(b->dist.data(), dist, b->dist.size(), cudaMemcpyDeviceToHost);
+        check_cuda("bake: download");
+        b->pyramid_base = uint32_t(render_res);
+        b->finalize();
+        *out = b.release();
+        return NGPRT_OK;
+    } catch (const std::exception& e) {
+        ngprt_host::set_error(e.what());
+        return NGPRT_EINVAL;
+    }
+}

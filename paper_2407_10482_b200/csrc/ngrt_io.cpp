@@ -7,6 +7,7 @@
 // The parse mirrors load_baked's checks and error texts (with byte offsets) and
 // yields an ngprt_scene_desc whose pyramid levels and distance grid are the
 // file's own (512..32 and 256^3, baking.hpp:435-447).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -14,23 +15,7 @@
 #include <string>
 #include <vector>
 
-#include "ngprt_cuda.h"
-
-namespace ngprt_host {
-void set_error(const std::string& msg);  // ngprt_abi.cu (ngprt_last_error)
-}
-
-struct ngprt_baked {
-    ngprt_scene_desc desc{};
-    std::vector<uint64_t> keys;
-    std::vector<float> rows;
-    std::vector<float> fine[NGPRT_MAX_FINE_LEVELS];
-    std::vector<float> psi_w[3], psi_b[3];
-    std::vector<float> att;
-    std::vector<float> fmlp_w[2], fmlp_b[2];
-    std::vector<uint64_t> pyramid[NGPRT_PYRAMID_LEVELS];
-    std::vector<uint8_t> dist;
-};
+#include "baked.hpp"
 
 namespace {
 
@@ -194,25 +179,9 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
         if (inv && !saw[6]) throw std::runtime_error("load_baked: missing attention globals section");
         if (d.fusion_tag == NGPRT_FUSION_MLP && !saw[7])
             throw std::runtime_error("load_baked: missing fusion MLP section");
-        for (int k = 0; k < 2; ++k) {
-            d.fusion_mlp_w[k] = b->fmlp_w[k].empty() ? nullptr : b->fmlp_w[k].data();
-            d.fusion_mlp_b[k] = b->fmlp_b[k].empty() ? nullptr : b->fmlp_b[k].data();
-        }
 
-        d.n_coarse = b->keys.size();
-        d.coarse_keys = b->keys.data();
-        d.coarse_rows = b->rows.data();
-        for (uint32_t l = 0; l < L; ++l) d.fine_tables[l] = b->fine[l].data();
-        for (int k = 0; k < 3; ++k) {
-            d.psi_w[k] = b->psi_w[k].data();
-            d.psi_b[k] = b->psi_b[k].data();
-        }
-        d.att_globals = b->att.empty() ? nullptr : b->att.data();
-        d.occ_base_res = 512;
-        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) d.pyramid_words[k] = b->pyramid[k].data();
-        d.dist_res = 256;
-        d.dist_values = b->dist.data();
-        d.storage = NGPRT_STORAGE_AUTO;
+        b->pyramid_base = 512;
+        b->finalize();
         *out = b.release();
         return NGPRT_OK;
     } catch (const std::exception& e) {
@@ -235,3 +204,114 @@ ngprt_status ngprt_scene_load(const char* path, int device, ngprt_scene** out) {
 }
 
 }  // extern "C"
+
+namespace {
+void put_bytes(std::vector<unsigned char>& out, const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    out.insert(out.end(), b, b + n);
+}
+template <class V>
+void put_pod(std::vector<unsigned char>& out, const V& v) {
+    put_bytes(out, &v, sizeof v);
+}
+void put_section(std::vector<unsigned char>& out, uint32_t id, const std::vector<unsigned char>& p) {
+    put_pod(out, id);
+    put_pod(out, uint64_t(p.size()));
+    put_bytes(out, p.data(), p.size());
+    put_pod(out, ngprt_crc32(p.data(), p.size(), 0));
+}
+}  // namespace
+
+extern "C" ngprt_status ngprt_baked_save(const ngprt_baked* b, const char* path) {
+    // save_baked, baking.hpp:266-349 (coarse table lengths of the header are the
+    // EncodingConfig defaults: the render path does not use them).
+    if (!b || !path) {
+        ngprt_host::set_error("ngprt_baked_save: null argument");
+        return NGPRT_EINVAL;
+    }
+    const ngprt_scene_desc& d = b->desc;
+    if (d.occ_base_res != 512 || d.dist_res != 256 || !d.dist_values) {
+        ngprt_host::set_error("save_baked: the format fixes a 512 pyramid and a 256^3 distance grid");
+        return NGPRT_EINVAL;
+    }
+    const int L = int(d.L), w = 8 + 2 * L;
+    std::vector<unsigned char> out;
+    put_bytes(out, "NGRT", 4);
+    put_pod(out, kVersion);
+    const size_t header_start = out.size();
+    put_pod(out, uint32_t(d.L_C));
+    put_pod(out, uint32_t(L));
+    for (int l = 0; l < L; ++l) put_pod(out, uint32_t(d.fine_res[l]));
+    const int cres[kCoarseLevels] = {16, 32, 64, 128, 256, 512};
+    for (int k = 0; k < kCoarseLevels; ++k) {
+        const uint64_t corners = uint64_t(cres[k] + 1) * (cres[k] + 1) * (cres[k] + 1);
+        put_pod(out, corners < (uint64_t(1) << 21) ? corners : (uint64_t(1) << 21));
+    }
+    for (int l = 0; l < L; ++l) put_pod(out, uint64_t(d.fine_table_len[l]));
+    put_pod(out, uint8_t(d.fusion_tag));
+    while ((out.size() - header_start) % 8 != 0) out.push_back(0);
+    {
+        std::vector<size_t> order(d.n_coarse);
+        for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+        std::sort(order.begin(), order.end(),
+                  [&](size_t x, size_t y) { return d.coarse_keys[x] < d.coarse_keys[y]; });
+        std::vector<unsigned char> p;
+        put_pod(p, uint64_t(d.n_coarse));
+        for (size_t i : order) {
+            put_pod(p, uint64_t(d.coarse_keys[i]));
+            put_bytes(p, d.coarse_rows + i * w, sizeof(float) * w);
+        }
+        put_section(out, 1, p);
+    }
+    {
+        std::vector<unsigned char> p;
+        for (int l = 0; l < L; ++l) put_bytes(p, d.fine_tables[l], d.fine_table_len[l] * 8 * sizeof(float));
+        put_section(out, 2, p);
+    }
+    {
+        std::vector<unsigned char> p;
+        const uint32_t dims[4] = {23, 64, 64, 3};
+        put_pod(p, uint32_t(4));
+        for (uint32_t v : dims) put_pod(p, v);
+        for (int k = 0; k < 3; ++k) {
+            put_bytes(p, d.psi_w[k], sizeof(float) * dims[k] * dims[k + 1]);
+            put_bytes(p, d.psi_b[k], sizeof(float) * dims[k + 1]);
+        }
+        put_section(out, 3, p);
+    }
+    {
+        std::vector<unsigned char> p;
+        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) {
+            const size_t res = size_t(512) >> k;
+            put_bytes(p, d.pyramid_words[k], ((res * res * res + 63) / 64) * 8);
+        }
+        put_section(out, 4, p);
+    }
+    {
+        std::vector<unsigned char> p;
+        put_bytes(p, d.dist_values, size_t(256) * 256 * 256);
+        put_section(out, 5, p);
+    }
+    if (d.fusion_tag == NGPRT_FUSION_SHARED_ATT_INV || d.fusion_tag == NGPRT_FUSION_SEPARATE_ATT_INV) {
+        std::vector<unsigned char> p;
+        put_bytes(p, d.att_globals, sizeof(float) * 2 * L);
+        put_section(out, 6, p);
+    }
+    if (d.fusion_tag == NGPRT_FUSION_MLP) {
+        std::vector<unsigned char> p;
+        const uint32_t dims[3] = {uint32_t(8 * L), 64, 8};
+        put_pod(p, uint32_t(3));
+        for (uint32_t v : dims) put_pod(p, v);
+        for (int k = 0; k < 2; ++k) {
+            put_bytes(p, d.fusion_mlp_w[k], sizeof(float) * dims[k] * dims[k + 1]);
+            put_bytes(p, d.fusion_mlp_b[k], sizeof(float) * dims[k + 1]);
+        }
+        put_section(out, 7, p);
+    }
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "wb"), &std::fclose);
+    if (!f || std::fwrite(out.data(), 1, out.size(), f.get()) != out.size()) {
+        ngprt_host::set_error(std::string("save_baked: cannot write ") + path);
+        return NGPRT_EINVAL;
+    }
+    return NGPRT_OK;
+}

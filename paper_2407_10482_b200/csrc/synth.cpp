@@ -380,6 +380,120 @@ ngprt_status ngprt_synth_create(const ngprt_synth_params* p, ngprt_synth** out) 
 
 const char* ngprt_synth_last_error(void) { return g_synth_err.c_str(); }
 
+}  // extern "C"
+
+struct ngprt_synth_model {
+    ngprt_model_desc desc{};
+    std::vector<float> coarse[6];
+    std::vector<float> aux_w[2], aux_b[2];
+    std::vector<float> fine[NGPRT_MAX_FINE_LEVELS];
+    std::vector<float> psi_w[3], psi_b[3];
+    std::vector<float> att, fmlp_w[2], fmlp_b[2];
+    std::vector<uint64_t> train;
+    uint32_t train_res = 0;
+};
+
+namespace {
+// TinyMlp::init (nn.hpp:154-173): He-uniform hidden, Xavier-uniform output, zero bias.
+void tiny_mlp_init(const std::vector<int>& widths, Rng& rng, std::vector<float>* w,
+                   std::vector<float>* b) {
+    const int n = int(widths.size()) - 1;
+    for (int k = 0; k < n; ++k) {
+        const int in = widths[k], o = widths[k + 1];
+        const double bound = (k + 1 < n) ? std::sqrt(6.0 / in) : std::sqrt(6.0 / (in + o));
+        w[k].resize(size_t(in) * o);
+        for (auto& v : w[k]) v = float(rng.uniform(-bound, bound));
+        b[k].assign(size_t(o), 0.f);
+    }
+}
+}  // namespace
+
+extern "C" {
+
+ngprt_status ngprt_synth_model_create(const ngprt_synth_params* p, ngprt_synth_model** out) {
+    *out = nullptr;
+    try {
+        if (p->L < 1 || p->L > NGPRT_MAX_FINE_LEVELS) throw std::invalid_argument("synth model: L in 1..4");
+        auto m = std::make_unique<ngprt_synth_model>();
+        const int L = int(p->L);
+        char name[33];
+        std::memcpy(name, p->occupancy, 32);
+        name[32] = 0;
+        auto rnd = [&](float v) { return p->fp16_exact ? round_fp16(v) : v; };
+        m->train_res = p->occ_base_res;
+        m->train = scene_occupancy(make_boxes(name, p->scene_seed, p->n_boxes), int(p->occ_base_res)).words;
+        ngprt_model_desc& d = m->desc;
+        d.L = p->L;
+        d.L_C = p->L_C;
+        const uint32_t cres[6] = {16, 32, 64, 128, 256, 512};  // EncodingConfig (hash_grid.hpp:125)
+        d.coarse_table_len = uint64_t(1) << 21;
+        Rng crng(p->coarse_seed);
+        for (int k = 0; k < 6; ++k) {
+            d.coarse_res[k] = cres[k];
+            const uint64_t corners = uint64_t(cres[k] + 1) * (cres[k] + 1) * (cres[k] + 1);
+            const uint64_t len = corners <= d.coarse_table_len ? corners : d.coarse_table_len;
+            m->coarse[k].resize(len * 4);
+            for (auto& v : m->coarse[k]) v = rnd(float(crng.uniform(-p->feat_scale, p->feat_scale)));
+            d.coarse_tables[k] = m->coarse[k].data();
+        }
+        Rng arng(p->psi_seed + 3);
+        tiny_mlp_init({24, 64, 8 + 2 * L}, arng, m->aux_w, m->aux_b);
+        for (int k = 0; k < 2; ++k) {
+            for (auto& v : m->aux_w[k]) v = rnd(v);
+            d.aux_w[k] = m->aux_w[k].data();
+            d.aux_b[k] = m->aux_b[k].data();
+        }
+        // density offset on the sigma channel so the cull keeps a mix of voxels
+        m->aux_b[1][0] = rnd(float(0.5 * (p->sigma_lo + p->sigma_hi)));
+        Rng frng(p->table_seed);
+        for (int l = 0; l < L; ++l) {
+            const uint32_t res = 1024u << l;
+            const uint64_t corners = uint64_t(res + 1) * (res + 1) * (res + 1);
+            d.fine_res[l] = res;
+            d.fine_hashed[l] = corners <= p->fine_table_len ? 0 : 1;
+            d.fine_table_len[l] = corners <= p->fine_table_len ? corners : p->fine_table_len;
+            m->fine[l].resize(d.fine_table_len[l] * 8);
+            for (auto& v : m->fine[l]) v = rnd(float(frng.uniform(-p->feat_scale, p->feat_scale)));
+            d.fine_tables[l] = m->fine[l].data();
+        }
+        Rng prng(p->psi_seed);
+        tiny_mlp_init({23, 64, 64, 3}, prng, m->psi_w, m->psi_b);
+        for (int k = 0; k < 3; ++k) {
+            for (auto& v : m->psi_w[k]) v = rnd(v);
+            d.psi_w[k] = m->psi_w[k].data();
+            d.psi_b[k] = m->psi_b[k].data();
+        }
+        d.fusion_tag = uint8_t(p->fusion_tag);
+        Rng grng(p->coarse_seed + 0x5bd1e995ull);
+        m->att.resize(size_t(2) * L);
+        for (auto& v : m->att) v = rnd(float(grng.uniform(-p->att_scale, p->att_scale)));
+        d.att_globals = m->att.data();
+        if (p->fusion_tag == NGPRT_FUSION_MLP) {
+            Rng mrng(p->psi_seed + 2);
+            tiny_mlp_init({8 * L, 64, 8}, mrng, m->fmlp_w, m->fmlp_b);
+            for (int k = 0; k < 2; ++k) {
+                for (auto& v : m->fmlp_w[k]) v = rnd(v);
+                d.fusion_mlp_w[k] = m->fmlp_w[k].data();
+                d.fusion_mlp_b[k] = m->fmlp_b[k].data();
+            }
+        }
+        *out = m.release();
+        return NGPRT_OK;
+    } catch (const std::exception& e) {
+        g_synth_err = e.what();
+        return NGPRT_EINVAL;
+    }
+}
+
+const ngprt_model_desc* ngprt_synth_model_desc(const ngprt_synth_model* m) { return &m->desc; }
+
+const uint64_t* ngprt_synth_model_train_words(const ngprt_synth_model* m, uint32_t* train_res) {
+    if (train_res) *train_res = m->train_res;
+    return m->train.data();
+}
+
+void ngprt_synth_model_destroy(ngprt_synth_model* m) { delete m; }
+
 const ngprt_scene_desc* ngprt_synth_desc(const ngprt_synth* s) { return &s->desc; }
 
 void ngprt_synth_destroy(ngprt_synth* s) { delete s; }

@@ -125,21 +125,50 @@ class SynthScene:
         self.close()
 
 
-class BakedFile:
-    """A baked scene read from the reference's `.ngrt` file (load_baked,
-    baking.hpp:351-485) on the host: CRC-checked sections, the file's own
-    512..32 pyramid and 256^3 distance grid. Pass it to Scene() to upload."""
+def _view(ptr, n, dtype):
+    if n == 0:
+        return np.zeros(0, dtype)
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dtype))),
+                                 shape=(int(n),))
 
-    def __init__(self, path):
-        h = C.c_void_p()
-        check(lib().ngprt_baked_load(str(path).encode(), C.byref(h)), "ngprt_baked_load")
-        self._h = h
-        self.desc_ptr = lib().ngprt_baked_desc(h)
+
+class BakedFile:
+    """A host BakedScene (baking.hpp:55-64): read from the reference's `.ngrt`
+    file (load_baked, baking.hpp:351-485; CRC-checked sections, the file's own
+    512..32 pyramid and 256^3 distance grid) or produced by bake(). Pass it to
+    Scene() to upload; save() writes the `.ngrt` file (save_baked, :266-349)."""
+
+    def __init__(self, path=None, *, _handle=None):
+        if _handle is None:
+            h = C.c_void_p()
+            check(lib().ngprt_baked_load(str(path).encode(), C.byref(h)), "ngprt_baked_load")
+            _handle = h
+        self._h = _handle
+        self.desc_ptr = lib().ngprt_baked_desc(self._h)
         self.desc: SceneDesc = self.desc_ptr.contents
 
     @property
     def L(self):
         return int(self.desc.L)
+
+    def save(self, path) -> None:
+        check(lib().ngprt_baked_save(self._h, str(path).encode()), "ngprt_baked_save")
+
+    # numpy views over the owned arrays (valid while self is alive)
+    def coarse_keys(self):
+        return _view(self.desc.coarse_keys, self.desc.n_coarse, np.uint64)
+
+    def coarse_rows(self):
+        w = 8 + 2 * self.L
+        return _view(self.desc.coarse_rows, self.desc.n_coarse * w, np.float32).reshape(-1, w)
+
+    def pyramid_words(self, k):
+        r = int(self.desc.occ_base_res) >> k
+        return _view(self.desc.pyramid_words[k], (r ** 3 + 63) // 64, np.uint64)
+
+    def dist_values(self):
+        r = int(self.desc.dist_res)
+        return _view(self.desc.dist_values, r ** 3, np.uint8)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -148,6 +177,61 @@ class BakedFile:
 
     def __del__(self):
         self.close()
+
+
+class SynthModel:
+    """Seeded synthetic trained NgpRtModel (model.hpp:27-107) plus its training
+    occupancy grid (ngprt_synth_model_*): the bake input. Same overrides as
+    SynthScene (occupancy, occ_base_res = training resolution, L, L_C, ...)."""
+
+    def __init__(self, **overrides):
+        p = SynthParams()
+        lib().ngprt_synth_default_params(C.byref(p))
+        for k, v in overrides.items():
+            if k not in SCENE_KEYS:
+                continue
+            if k == "occupancy":
+                v = v.encode()
+            if k == "fusion_tag" and isinstance(v, str):
+                v = _abi.FUSION[v]
+            setattr(p, k, v)
+        self.params = p
+        h = C.c_void_p()
+        if lib().ngprt_synth_model_create(C.byref(p), C.byref(h)) != _abi.OK:
+            raise ValueError("ngprt_synth_model_create: " +
+                             lib().ngprt_synth_last_error().decode(errors="replace"))
+        self._h = h
+        self.desc_ptr = lib().ngprt_synth_model_desc(h)
+        self.desc = self.desc_ptr.contents
+        res = C.c_uint32()
+        self.train_ptr = lib().ngprt_synth_model_train_words(h, C.byref(res))
+        self.train_res = int(res.value)
+
+    def train_words(self):
+        return _view(self.train_ptr, (self.train_res ** 3 + 63) // 64, np.uint64)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ngprt_synth_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def bake(model, train_words=None, train_res: int | None = None, *, cull_step: float = 0.0,
+         cull_alpha_thresh: float = 0.005, dilate_voxels: int = 1, device: int = 0) -> BakedFile:
+    """bake(model, train_grid, BakeOptions) (baking.hpp:107-202) on the GPU.
+    `model` is a SynthModel (or anything with desc_ptr / train_words()); the
+    result is a host BakedFile, bit-identical to the reference's bake."""
+    if train_words is None:
+        train_words, train_res = model.train_words(), model.train_res
+    words = np.ascontiguousarray(train_words, dtype=np.uint64)
+    o = _abi.BakeOpts(cull_step, cull_alpha_thresh, dilate_voxels, 0)
+    h = C.c_void_p()
+    check(lib().ngprt_bake(model.desc_ptr, words.ctypes.data, int(train_res), C.byref(o), device,
+                           C.byref(h)), "ngprt_bake")
+    return BakedFile(_handle=h)
 
 
 def cameras(n: int, width: int, height: int, radius: float = 2.9):

@@ -89,3 +89,44 @@ def random_grid_words(ng, res: int, density: float, seed: int) -> np.ndarray:
     words = np.zeros((n + 63) // 64, np.uint64)
     words.view(np.uint8)[: packed.size] = packed
     return words
+
+
+# Bake cases (baking.hpp:107-202): a seeded synthetic NgpRtModel (SynthModel)
+# and its training occupancy. `scene` keys go to ngprt_synth_model_create
+# (occ_base_res = training resolution); sigma_lo = sigma_hi sets the aux
+# decoder's density bias so the cull keeps roughly half the voxels. Together
+# they cover every fusion mode including the MLP ablation, L = 2..4, L_C above,
+# equal to and below the training resolution, dilation 0..2, non-default
+# cull step and threshold.
+BAKE_CASES = [
+    dict(name="toy_sepv_up2", scene=dict(occupancy="toy", occ_base_res=64, L=2, L_C=128,
+                                         fine_table_len=1 << 16, sigma_lo=-0.5, sigma_hi=-0.5),
+         opts=dict()),
+    dict(name="bench_sharedinv_eq", scene=dict(occupancy="bench", occ_base_res=64, L=3, L_C=64,
+                                               fine_table_len=1 << 15, fusion_tag="shared_att_inv",
+                                               sigma_lo=-0.5, sigma_hi=-0.5),
+         opts=dict()),
+    dict(name="toy_sum_down2_dil2", scene=dict(occupancy="toy", occ_base_res=128, L=2, L_C=64,
+                                               fine_table_len=1 << 14, fusion_tag="sum",
+                                               sigma_lo=0.0, sigma_hi=0.0),
+         opts=dict(dilate_voxels=2)),
+    dict(name="toy_mlp_l4_down2_nodil", scene=dict(occupancy="toy", occ_base_res=64, L=4, L_C=32,
+                                                   fine_table_len=1 << 12, fusion_tag="mlp",
+                                                   sigma_lo=-0.5, sigma_hi=-0.5),
+         opts=dict(dilate_voxels=0)),
+    dict(name="blob_sepinv_up4_step", scene=dict(occupancy="blob", occ_base_res=32, L=2, L_C=128,
+                                                 fine_table_len=1 << 13,
+                                                 fusion_tag="separate_att_inv",
+                                                 sigma_lo=-1.0, sigma_hi=-1.0),
+         opts=dict(cull_step=0.01, cull_alpha_thresh=0.01)),
+    dict(name="bench_sharedv_l2", scene=dict(occupancy="bench", occ_base_res=64, L=2, L_C=128,
+                                             fine_table_len=1 << 16, fusion_tag="shared_att_v",
+                                             sigma_lo=-0.5, sigma_hi=-0.5),
+         opts=dict()),
+]
+
+
+def bake_opts(o: dict):
+    from paper_2407_10482_b200 import _abi
+    return _abi.BakeOpts(o.get("cull_step", 0.0), o.get("cull_alpha_thresh", 0.005),
+                         o.get("dilate_voxels", 1), 0)

@@ -116,6 +116,8 @@ def ref():
         L.ref_base_step.restype = C.c_double
         L.ref_save_baked.restype = C.c_int
         L.ref_save_baked.argtypes = [P, C.c_char_p]
+        L.ref_bake.restype = C.c_int
+        L.ref_bake.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_char_p]
         _ref = L
     return _ref
 
