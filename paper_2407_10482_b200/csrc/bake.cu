@@ -21,12 +21,20 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include <mutex>
+#include <thread>
 
 #include "baked.hpp"
 #include "render.cuh"
@@ -121,8 +129,27 @@ __device__ void evaluate_corner(const DevModel& M, int cx, int cy, int cz, float
     }
 }
 
+// Corner rows evaluated once per distinct corner (the reference's CornerCache,
+// model.hpp:113-150): a bitmap of the corners present, the exclusive prefix
+// count of each 32-bit word and the rows in key order; rank lookup = 2 loads.
+struct CornerTable {
+    const uint32_t* marks;
+    const uint32_t* offsets;
+    const float* rows;
+    unsigned long long r1;
+    int W;
+};
+
+__device__ __forceinline__ const float* corner_row(const CornerTable& T, int x, int y, int z) {
+    const unsigned long long key =
+        (unsigned long long)x + T.r1 * ((unsigned long long)y + T.r1 * (unsigned long long)z);
+    const uint32_t w = __ldg(T.marks + (key >> 5));
+    const uint32_t rank = __ldg(T.offsets + (key >> 5)) + __popc(w & ((1u << (key & 31)) - 1u));
+    return T.rows + size_t(rank) * T.W;
+}
+
 // sigma_pre of decode_point (model.hpp:195-239) at x: only channel 0 of the fuse.
-__device__ float decode_sigma_pre(const DevModel& M, const float x[3],
+__device__ float decode_sigma_pre(const DevModel& M, const CornerTable& T, const float x[3],
                                   const unsigned long long* tab) {
     int cb[3];
     float cf[3];
@@ -133,9 +160,8 @@ __device__ float decode_sigma_pre(const DevModel& M, const float x[3],
         const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
         const float w = ((dx ? cf[0] : 1.0f - cf[0]) * (dy ? cf[1] : 1.0f - cf[1])) *
                         (dz ? cf[2] : 1.0f - cf[2]);
-        float row[16];
-        evaluate_corner(M, cb[0] + dx, cb[1] + dy, cb[2] + dz, row);
-        for (int i = 0; i < M.W; ++i) dec[i] += w * row[i];
+        const float* row = corner_row(T, cb[0] + dx, cb[1] + dy, cb[2] + dz);
+        for (int i = 0; i < M.W; ++i) dec[i] += w * __ldg(row + i);
     }
     float fine[NGPRT_MAX_FINE_LEVELS][8];
     for (int l = 0; l < M.L; ++l)
@@ -174,9 +200,36 @@ __device__ __forceinline__ bool bit_at(const uint32_t* g, int res, int x, int y,
     return (g[i >> 5] >> (i & 31)) & 1u;
 }
 
+// Training-voxel centre (baking.hpp:128-129).
+__device__ __forceinline__ void voxel_centre(size_t i, int tres, float c[3]) {
+    const int x = int(i % tres), y = int((i / tres) % tres), z = int(i / (size_t(tres) * tres));
+    const double vsz = 2.0 / tres;  // Roi::extent / tres
+    c[0] = float(-1.0 + (x + 0.5) * vsz);
+    c[1] = float(-1.0 + (y + 0.5) * vsz);
+    c[2] = float(-1.0 + (z + 0.5) * vsz);
+}
+
+// The L_C corners the cull's decodes read: the stencil corners of every
+// occupied training-voxel centre.
+__global__ void cull_marks_kernel(const DevModel M, const uint32_t* __restrict__ train, int tres,
+                                  uint32_t* marks) {
+    const size_t n = size_t(tres) * tres * tres;
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i >= n || !((train[i >> 5] >> (i & 31)) & 1u)) return;
+    float c[3], f;
+    int b[3];
+    voxel_centre(i, tres, c);
+    for (int a = 0; a < 3; ++a) stencil_axis(c[a], M.lc_h, M.L_C, b[a], f);
+    const size_t r1 = size_t(M.L_C) + 1;
+    for (int k = 0; k < 8; ++k) {
+        const size_t key = size_t(b[0] + (k & 1)) + r1 * (size_t(b[1] + ((k >> 1) & 1)) + r1 * size_t(b[2] + (k >> 2)));
+        atomicOr(marks + (key >> 5), 1u << (key & 31));
+    }
+}
+
 // (1) density cull: one thread per training voxel; 32 voxels -> one ballot word.
-__global__ void cull_kernel(const DevModel M, const uint32_t* __restrict__ train, int tres,
-                            double cull_step, double thresh, uint32_t* __restrict__ culled,
+__global__ void cull_kernel(const DevModel M, const CornerTable T, const uint32_t* __restrict__ train,
+                            int tres, double cull_step, double thresh, uint32_t* __restrict__ culled,
                             unsigned int* amb_n, uint32_t* amb_idx, float* amb_sigma, int amb_cap) {
     __shared__ unsigned long long tab[32];
     load_exp_table(tab);
@@ -185,11 +238,9 @@ __global__ void cull_kernel(const DevModel M, const uint32_t* __restrict__ train
     const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     bool keep = false;
     if (i < n && ((train[i >> 5] >> (i & 31)) & 1u)) {
-        const int x = int(i % tres), y = int((i / tres) % tres), z = int(i / (size_t(tres) * tres));
-        const double vsz = 2.0 / tres;  // Roi::extent / tres
-        const float c[3] = {float(-1.0 + (x + 0.5) * vsz), float(-1.0 + (y + 0.5) * vsz),
-                            float(-1.0 + (z + 0.5) * vsz)};
-        const float sigma = activate_density(decode_sigma_pre(M, c, tab), tab);
+        float c[3];
+        voxel_centre(i, tres, c);
+        const float sigma = activate_density(decode_sigma_pre(M, T, c, tab), tab);
         const double e = exp(-double(sigma) * cull_step);
         keep = 1.0 - e > thresh;
         if (fabs(e - (1.0 - thresh)) < 1e-12) {  // glibc exp may decide differently: host re-check
@@ -262,6 +313,23 @@ __global__ void corner_eval_kernel(const DevModel M, const unsigned long long* _
     for (int j = 0; j < M.W; ++j) rows[i * M.W + j] = row[j];
 }
 
+// Retained corner keys in ascending order (== the reference's z,y,x scan,
+// baking.hpp:167-175): per-word popcount -> exclusive scan -> scatter.
+__global__ void popcount_kernel(const uint32_t* __restrict__ marks, size_t nw, uint32_t* counts) {
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i < nw) counts[i] = __popc(marks[i]);
+    else if (i == nw) counts[i] = 0;
+}
+
+__global__ void scatter_keys_kernel(const uint32_t* __restrict__ marks, size_t nw,
+                                    const uint32_t* __restrict__ offsets,
+                                    unsigned long long* __restrict__ keys) {
+    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i >= nw) return;
+    uint32_t o = offsets[i];
+    for (uint32_t m = marks[i]; m; m &= m - 1) keys[o++] = (i << 5) + unsigned(__ffs(m) - 1);
+}
+
 unsigned blocks(size_t n, unsigned bs) { return unsigned((n + bs - 1) / bs); }
 size_t words32(size_t res) { return ((res * res * res + 63) / 64) * 2; }
 
@@ -272,24 +340,142 @@ using namespace ngprt_dev;
 
 namespace {
 
-struct DeviceBuffers {  // frees everything on scope exit
+// NGPRT_BAKE_PROFILE=1: per-phase wall times (device synchronised) on stderr.
+struct PhaseTimer {
+    bool on = std::getenv("NGPRT_BAKE_PROFILE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* name) {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[bake] %-14s %9.3f ms\n", name,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
+// Host <-> device copies of the large arrays (corner rows can be GBs; fine
+// tables and coarse tables are 100s of MB) through two pinned staging chunks
+// on a blocking stream (ordered with the legacy-stream kernels): the DMA of one
+// chunk overlaps a multi-threaded memcpy of the other, so pageable memory
+// moves at several times the speed of a plain cudaMemcpy from/to it.
+constexpr size_t kChunk = size_t(32) << 20;
+constexpr int kMaxThreads = 16;
+
+int copy_threads() {
+    static const int t = [] {
+        const char* e = std::getenv("NGPRT_COPY_THREADS");
+        const int v = e ? std::atoi(e) : 8;
+        return v < 1 ? 1 : (v > kMaxThreads ? kMaxThreads : v);
+    }();
+    return t;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    const int nt = bytes < (size_t(4) << 20) ? 1 : copy_threads();
+    const size_t part = (bytes / nt + 63) & ~size_t(63);
+    std::thread th[kMaxThreads - 1];
+    auto piece = [=](int t) {
+        const size_t a = std::min(bytes, t * part), b = std::min(bytes, (t + 1) * part);
+        if (b > a) std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    };
+    for (int t = 1; t < nt; ++t) th[t - 1] = std::thread(piece, t);
+    piece(0);
+    for (int t = 1; t < nt; ++t) th[t - 1].join();
+}
+
+struct Staging {
+    std::mutex mu;
+    void* buf[2] = {nullptr, nullptr};
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[2];
+    void init() {
+        if (st) return;
+        cudaStreamCreate(&st);
+        for (int i = 0; i < 2; ++i) {
+            cudaMallocHost(&buf[i], kChunk);
+            cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+        }
+    }
+};
+
+Staging& staging() {
+    static Staging s;
+    return s;
+}
+
+void d2h(void* dst, const void* src, size_t bytes) {
+    if (bytes < 4 * kChunk) {
+        cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+        return;
+    }
+    Staging& S = staging();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.init();
+    const size_t n = (bytes + kChunk - 1) / kChunk;
+    auto len = [&](size_t i) { return std::min(kChunk, bytes - i * kChunk); };
+    auto issue = [&](size_t i) {
+        cudaMemcpyAsync(S.buf[i & 1], static_cast<const char*>(src) + i * kChunk, len(i),
+                        cudaMemcpyDeviceToHost, S.st);
+        cudaEventRecord(S.ev[i & 1], S.st);
+    };
+    issue(0);
+    for (size_t i = 0; i < n; ++i) {
+        if (i + 1 < n) issue(i + 1);
+        cudaEventSynchronize(S.ev[i & 1]);
+        parallel_memcpy(static_cast<char*>(dst) + i * kChunk, S.buf[i & 1], len(i));
+    }
+}
+
+void h2d(void* dst, const void* src, size_t bytes) {
+    if (bytes < 4 * kChunk) {
+        cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+        return;
+    }
+    Staging& S = staging();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.init();
+    const size_t n = (bytes + kChunk - 1) / kChunk;
+    for (size_t i = 0; i < n; ++i) {
+        const size_t len = std::min(kChunk, bytes - i * kChunk);
+        if (i >= 2) cudaEventSynchronize(S.ev[i & 1]);  // chunk i-2's DMA has drained this buffer
+        parallel_memcpy(S.buf[i & 1], static_cast<const char*>(src) + i * kChunk, len);
+        cudaMemcpyAsync(static_cast<char*>(dst) + i * kChunk, S.buf[i & 1], len,
+                        cudaMemcpyHostToDevice, S.st);
+        cudaEventRecord(S.ev[i & 1], S.st);
+    }
+    cudaStreamSynchronize(S.st);
+}
+
+// Stream-ordered scratch from the device's default pool (kept mapped between
+// bakes: the release threshold is raised as for the renderer's scratch), all
+// freed on scope exit.
+struct DeviceBuffers {
     std::vector<void*> ptrs;
+    DeviceBuffers(int device) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = ~uint64_t(0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     ~DeviceBuffers() {
-        for (void* p : ptrs) cudaFree(p);
+        for (void* p : ptrs) cudaFreeAsync(p, 0);
+        cudaStreamSynchronize(0);
     }
     template <class T>
     T* alloc(size_t count) {
         void* p = nullptr;
-        const cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 16);
-        if (e != cudaSuccess) throw std::runtime_error(std::string("bake: cudaMalloc: ") + cudaGetErrorString(e));
-        cudaMemset(p, 0, count * sizeof(T) + 16);
+        const cudaError_t e = cudaMallocAsync(&p, count * sizeof(T) + 16, 0);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("bake: cudaMallocAsync: ") + cudaGetErrorString(e));
+        cudaMemsetAsync(p, 0, count * sizeof(T) + 16, 0);
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
     template <class T>
     T* upload(const T* h, size_t count) {
         T* d = alloc<T>(count);
-        cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice);
+        h2d(d, h, count * sizeof(T));
         return d;
     }
 };
@@ -300,8 +486,25 @@ void check_cuda(const char* what) {
 }
 
 void check_finite(const float* p, size_t n, const std::string& group) {
-    for (size_t i = 0; i < n; ++i)
-        if (!std::isfinite(p[i])) throw std::runtime_error("bake: non-finite parameter in group " + group);
+    const int nt = n < (size_t(1) << 20) ? 1 : copy_threads();
+    const size_t part = (n + nt - 1) / nt;
+    bool bad[kMaxThreads] = {};
+    std::thread th[kMaxThreads - 1];
+    auto piece = [&](int t) {
+        const size_t a = std::min(n, t * part), b = std::min(n, (t + 1) * part);
+        uint32_t acc = 0;  // exponent all-ones <=> inf/nan
+        for (size_t i = a; i < b; ++i) {
+            uint32_t u;
+            std::memcpy(&u, p + i, 4);
+            acc |= uint32_t((u & 0x7f800000u) == 0x7f800000u);
+        }
+        bad[t] = acc != 0;
+    };
+    for (int t = 1; t < nt; ++t) th[t - 1] = std::thread(piece, t);
+    piece(0);
+    for (int t = 1; t < nt; ++t) th[t - 1].join();
+    for (int t = 0; t < nt; ++t)
+        if (bad[t]) throw std::runtime_error("bake: non-finite parameter in group " + group);
 }
 
 }  // namespace
@@ -355,8 +558,9 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
             }
 
         // the model on the device
+        PhaseTimer pt;
         if (cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("bake: no CUDA device");
-        DeviceBuffers db;
+        DeviceBuffers db(device);
         DevModel M{};
         M.L = L;
         M.L_C = lc;
@@ -400,15 +604,51 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
             M.fmlp = db.upload(f.data(), f.size());
         }
 
+        pt.mark("upload");
+        // marks bitmap -> ascending keys + per-word exclusive counts (rank table)
+        auto compact = [&](const uint32_t* marks, size_t nw, uint32_t** offsets_out,
+                           unsigned long long** keys_out) -> uint32_t {
+            uint32_t* counts = db.alloc<uint32_t>(nw + 1);
+            uint32_t* offsets = db.alloc<uint32_t>(nw + 1);
+            popcount_kernel<<<blocks(nw + 1, 256), 256>>>(marks, nw, counts);
+            size_t scan_bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, offsets, nw + 1);
+            void* scan_tmp = db.alloc<uint8_t>(scan_bytes);
+            cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, offsets, nw + 1);
+            uint32_t n = 0;
+            cudaMemcpy(&n, offsets + nw, 4, cudaMemcpyDeviceToHost);
+            check_cuda("bake: corner keys");
+            unsigned long long* keys = db.alloc<unsigned long long>(n ? n : 1);
+            if (n) scatter_keys_kernel<<<blocks(nw, 256), 256>>>(marks, nw, offsets, keys);
+            *offsets_out = offsets;
+            *keys_out = keys;
+            return n;
+        };
+        const size_t r1 = size_t(lc) + 1;
+        const size_t nw = words32(r1);
+
         // (1) density cull at the training resolution, exact decisions
         const size_t tn = size_t(tres) * tres * tres;
+        CornerTable cull_table{};
         uint32_t* train = db.upload(reinterpret_cast<const uint32_t*>(train_words), words32(tres));
         uint32_t* culled = db.alloc<uint32_t>(words32(tres));
         unsigned int* amb_n = db.alloc<unsigned int>(1);
         const int amb_cap = 1 << 16;
         uint32_t* amb_idx = db.alloc<uint32_t>(amb_cap);
         float* amb_sigma = db.alloc<float>(amb_cap);
-        cull_kernel<<<blocks(tn, 128), 128>>>(M, train, int(tres), cull_step, thresh, culled, amb_n,
+        {
+            uint32_t* cmarks = db.alloc<uint32_t>(nw);
+            cull_marks_kernel<<<blocks(tn, 256), 256>>>(M, train, int(tres), cmarks);
+            uint32_t* coffsets;
+            unsigned long long* ckeys;
+            const uint32_t nc = compact(cmarks, nw, &coffsets, &ckeys);
+            float* crows = db.alloc<float>(size_t(nc ? nc : 1) * W);
+            if (nc) corner_eval_kernel<<<blocks(nc, 128), 128>>>(M, ckeys, nc, crows);
+            check_cuda("bake: cull corners");
+            pt.mark("cull_corners");
+            cull_table = CornerTable{cmarks, coffsets, crows, (unsigned long long)r1, W};
+        }
+        cull_kernel<<<blocks(tn, 128), 128>>>(M, cull_table, train, int(tres), cull_step, thresh, culled, amb_n,
                                               amb_idx, amb_sigma, amb_cap);
         check_cuda("bake: cull");
         unsigned int n_amb = 0;
@@ -427,6 +667,7 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
             }
             cudaMemcpy(culled, words.data(), words.size() * 4, cudaMemcpyHostToDevice);
         }
+        pt.mark("cull");
         for (int i = 0; i < dilate; ++i) {
             uint32_t* d2 = db.alloc<uint32_t>(words32(tres));
             dilate_kernel<<<blocks(tn, 256), 256>>>(culled, int(tres), d2);
@@ -434,6 +675,7 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
         }
         check_cuda("bake: dilate");
 
+        pt.mark("dilate");
         // (2) render grid, pyramid, distance grid (baking.hpp:137-144)
         const int f = render_res / int(tres);
         uint32_t* levels[NGPRT_PYRAMID_LEVELS];
@@ -450,6 +692,7 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
         launch_distance_grid(levels[1], 256, ta, tb, dist, nullptr);
         check_cuda("bake: pyramid / distance grid");
 
+        pt.mark("grids");
         // (3) corner retention on the L_C grid and corner evaluation
         uint32_t* occ_lc = culled;
         int r = int(tres);
@@ -466,28 +709,26 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
                 r /= 2;
             }
         }
-        const size_t r1 = size_t(lc) + 1;
-        uint32_t* marks = db.alloc<uint32_t>(words32(r1));
+        uint32_t* marks = db.alloc<uint32_t>(nw);
         corner_marks_kernel<<<blocks(size_t(lc) * lc * lc, 256), 256>>>(occ_lc, lc, marks);
         check_cuda("bake: corner marks");
-        std::vector<uint32_t> hmarks(words32(r1));
-        cudaMemcpy(hmarks.data(), marks, hmarks.size() * 4, cudaMemcpyDeviceToHost);
+        uint32_t* offsets;
+        unsigned long long* dkeys;
+        const uint32_t n_keys = compact(marks, nw, &offsets, &dkeys);
         auto b = std::make_unique<ngprt_baked>();
-        const size_t ncorner = r1 * r1 * r1;
-        for (size_t wi = 0; wi < hmarks.size(); ++wi)  // key order == the reference's z,y,x scan
-            for (uint32_t m = hmarks[wi]; m; m &= m - 1) {
-                const size_t key = (wi << 5) + size_t(__builtin_ctz(m));
-                if (key < ncorner) b->keys.push_back(key);
-            }
-        b->rows.resize(b->keys.size() * W);
-        if (!b->keys.empty()) {
-            unsigned long long* dkeys = db.upload(reinterpret_cast<const unsigned long long*>(b->keys.data()), b->keys.size());
+        b->keys.resize(n_keys);
+        b->rows.resize(size_t(n_keys) * W);
+        pt.mark("keys");
+        if (n_keys) {
             float* drows = db.alloc<float>(b->rows.size());
-            corner_eval_kernel<<<blocks(b->keys.size(), 128), 128>>>(M, dkeys, b->keys.size(), drows);
+            corner_eval_kernel<<<blocks(n_keys, 128), 128>>>(M, dkeys, n_keys, drows);
             check_cuda("bake: corner evaluation");
-            cudaMemcpy(b->rows.data(), drows, b->rows.size() * 4, cudaMemcpyDeviceToHost);
+            pt.mark("corner_kernel");
+            d2h(b->keys.data(), dkeys, size_t(n_keys) * 8);
+            d2h(b->rows.data(), drows, b->rows.size() * 4);
         }
 
+        pt.mark("rows_d2h");
         // (4) assemble the BakedScene (verbatim carry-over, baking.hpp:176-200)
         ngprt_scene_desc& d = b->desc;
         d.L = uint32_t(L);
@@ -497,7 +738,8 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
             d.fine_res[l] = md->fine_res[l];
             d.fine_table_len[l] = md->fine_table_len[l];
             d.fine_hashed[l] = md->fine_hashed[l];
-            b->fine[l].assign(md->fine_tables[l], md->fine_tables[l] + md->fine_table_len[l] * 8);
+            b->fine[l].resize(md->fine_table_len[l] * 8);
+            parallel_memcpy(b->fine[l].data(), md->fine_tables[l], b->fine[l].size() * 4);
         }
         const int pw[4] = {23, 64, 64, 3};
         for (int k = 0; k < 3; ++k) {
@@ -515,13 +757,14 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
         for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k) {
             const size_t res = size_t(render_res) >> k;
             b->pyramid[k].resize((res * res * res + 63) / 64);
-            cudaMemcpy(b->pyramid[k].data(), levels[k], b->pyramid[k].size() * 8, cudaMemcpyDeviceToHost);
+            d2h(b->pyramid[k].data(), levels[k], b->pyramid[k].size() * 8);
         }
         b->dist.resize(size_t(256) * 256 * 256);
-        cudaMemcpy(b->dist.data(), dist, b->dist.size(), cudaMemcpyDeviceToHost);
+        d2h(b->dist.data(), dist, b->dist.size());
         check_cuda("bake: download");
         b->pyramid_base = uint32_t(render_res);
         b->finalize();
+        pt.mark("assemble");
         *out = b.release();
         return NGPRT_OK;
     } catch (const std::exception& e) {

@@ -3,21 +3,61 @@
 // ngprt_scene_desc via ngprt_baked_desc().
 #pragma once
 
+#include <sys/mman.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <new>
 #include <string>
 #include <vector>
 
 #include "ngprt_cuda.h"
 
+// Large host arrays of a BakedScene: uninitialised on resize (the bake and the
+// loader overwrite every element) and 2 MiB-aligned with transparent huge pages
+// advised, so filling a multi-GB corner-row array is not dominated by page
+// faults and zero-fill.
+template <class T>
+struct HostBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() { std::free(p); }
+    void resize(size_t m) {  // contents are not preserved
+        std::free(p);
+        p = nullptr;
+        n = m;
+        if (!m) return;
+        constexpr size_t kHuge = size_t(2) << 20;
+        const size_t bytes = (m * sizeof(T) + kHuge - 1) / kHuge * kHuge;
+        p = static_cast<T*>(std::aligned_alloc(kHuge, bytes));
+        if (!p) throw std::bad_alloc();
+        madvise(p, bytes, MADV_HUGEPAGE);
+    }
+    void assign(const T* a, const T* b) {
+        resize(size_t(b - a));
+        if (n) std::memcpy(p, a, n * sizeof(T));
+    }
+    T* data() { return p; }
+    const T* data() const { return p; }
+    size_t size() const { return n; }
+    bool empty() const { return n == 0; }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
+};
+
 struct ngprt_baked {
     ngprt_scene_desc desc{};
-    std::vector<uint64_t> keys;
-    std::vector<float> rows;
-    std::vector<float> fine[NGPRT_MAX_FINE_LEVELS];
+    HostBuf<uint64_t> keys;
+    HostBuf<float> rows;
+    HostBuf<float> fine[NGPRT_MAX_FINE_LEVELS];
     std::vector<float> psi_w[3], psi_b[3];
     std::vector<float> att;
     std::vector<float> fmlp_w[2], fmlp_b[2];
-    std::vector<uint64_t> pyramid[NGPRT_PYRAMID_LEVELS];
-    std::vector<uint8_t> dist;
+    HostBuf<uint64_t> pyramid[NGPRT_PYRAMID_LEVELS];
+    HostBuf<uint8_t> dist;
     uint32_t pyramid_base = 512;
 
     // Points desc at the owned arrays (call after filling them).
