@@ -51,12 +51,13 @@ struct DevModel {
     float ch[kCoarseLevels];
     int cdirect[kCoarseLevels];
     unsigned long long clen[kCoarseLevels];
+    unsigned long long cmask[kCoarseLevels];  // len - 1 for a power-of-two hashed length, else 0
     const float* ctab[kCoarseLevels];
-    const float* aux;  // W0 (64x24) b0 (64) W1 (Wx64) b1 (W)
     int fine_res[NGPRT_MAX_FINE_LEVELS];
     float fine_h[NGPRT_MAX_FINE_LEVELS];
     int fine_hashed[NGPRT_MAX_FINE_LEVELS];
     unsigned long long fine_len[NGPRT_MAX_FINE_LEVELS];
+    unsigned long long fine_mask[NGPRT_MAX_FINE_LEVELS];
     const float* fine[NGPRT_MAX_FINE_LEVELS];
     int fusion;
     float att_w[2 * NGPRT_MAX_FINE_LEVELS];
@@ -73,8 +74,9 @@ __device__ __forceinline__ void stencil_axis(float x, float h, int res, int& bas
     frac = u - float(i);
 }
 
-// HashLevel::hash_index, hash_grid.hpp:83-94
-__device__ __forceinline__ unsigned long long hash_index(int res, unsigned long long len, int hashed,
+// HashLevel::hash_index, hash_grid.hpp:83-94 (h % len == h & (len-1) for a power of two)
+__device__ __forceinline__ unsigned long long hash_index(int res, unsigned long long len,
+                                                         unsigned long long mask, int hashed,
                                                          int x, int y, int z) {
     if (!hashed) {
         const unsigned long long r1 = (unsigned long long)res + 1;
@@ -83,14 +85,14 @@ __device__ __forceinline__ unsigned long long hash_index(int res, unsigned long 
     const unsigned long long h = (unsigned long long)x * 1ull ^
                                  (unsigned long long)y * 2654435761ull ^
                                  (unsigned long long)z * 805459861ull;
-    return h % len;
+    return mask ? (h & mask) : h % len;
 }
 
 // HashLevel::interp (hash_grid.hpp:97-104) of a D-wide table at x.
 template <int D>
 __device__ __forceinline__ void interp(const float* __restrict__ tab, int res, float h,
-                                       unsigned long long len, int hashed, const float x[3],
-                                       float* out) {
+                                       unsigned long long len, unsigned long long mask, int hashed,
+                                       const float x[3], float* out) {
     int b[3];
     float f[3];
     for (int a = 0; a < 3; ++a) stencil_axis(x[a], h, res, b[a], f[a]);
@@ -99,33 +101,54 @@ __device__ __forceinline__ void interp(const float* __restrict__ tab, int res, f
         const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
         const float w = ((dx ? f[0] : 1.0f - f[0]) * (dy ? f[1] : 1.0f - f[1])) *
                         (dz ? f[2] : 1.0f - f[2]);
-        const float* row = tab + hash_index(res, len, hashed, b[0] + dx, b[1] + dy, b[2] + dz) * D;
+        const float4* row = reinterpret_cast<const float4*>(
+            tab + hash_index(res, len, mask, hashed, b[0] + dx, b[1] + dy, b[2] + dz) * D);
 #pragma unroll
-        for (int c = 0; c < D; ++c) out[c] += w * __ldg(row + c);
+        for (int q = 0; q < D / 4; ++q) {  // rows are 16-byte aligned (D = 4 or 8)
+            const float4 v = __ldg(row + q);
+            out[4 * q + 0] += w * v.x;
+            out[4 * q + 1] += w * v.y;
+            out[4 * q + 2] += w * v.z;
+            out[4 * q + 3] += w * v.w;
+        }
     }
 }
 
+// The aux decoder's weights as a kernel parameter (10.5 KB, constant bank 0):
+// with the loops below fully unrolled every weight is an FMUL operand read
+// from the constant bank, no load instruction per multiply-add.
+struct AuxWeights {
+    float w0[64 * 24];
+    float b0[64];
+    float w1[16 * 64];
+    float b1[16];
+};
+
 // NgpRtModel::evaluate_corner (model.hpp:71-87): encode_coarse at the corner
 // position (corner_to_world, hash_grid.hpp:28-31) through the aux MLP.
-__device__ void evaluate_corner(const DevModel& M, int cx, int cy, int cz, float* out) {
+template <int W>
+__device__ __forceinline__ void evaluate_corner(const DevModel& M, const AuxWeights& A, int cx,
+                                                int cy, int cz, float* out) {
     const float pos[3] = {-1.0f + 2.0f * (float(cx) / float(M.L_C)),
                           -1.0f + 2.0f * (float(cy) / float(M.L_C)),
                           -1.0f + 2.0f * (float(cz) / float(M.L_C))};
     float feat[24];
+#pragma unroll
     for (int k = 0; k < kCoarseLevels; ++k)
-        interp<4>(M.ctab[k], M.cres[k], M.ch[k], M.clen[k], !M.cdirect[k], pos, feat + 4 * k);
+        interp<4>(M.ctab[k], M.cres[k], M.ch[k], M.clen[k], M.cmask[k], !M.cdirect[k], pos,
+                  feat + 4 * k);
     // TinyMlp::forward (nn.hpp:175-196), hidden unit by unit; the output layer
     // accumulates in the same c-order as the reference's inner loop.
-    const float* W0 = M.aux;
-    const float* B0 = W0 + 64 * 24;
-    const float* W1 = B0 + 64;
-    const float* B1 = W1 + M.W * 64;
-    for (int j = 0; j < M.W; ++j) out[j] = __ldg(B1 + j);
+#pragma unroll
+    for (int j = 0; j < W; ++j) out[j] = A.b1[j];
+#pragma unroll
     for (int r = 0; r < 64; ++r) {
-        float h = __ldg(B0 + r);
-        for (int c = 0; c < 24; ++c) h += __ldg(W0 + r * 24 + c) * feat[c];
+        float h = A.b0[r];
+#pragma unroll
+        for (int c = 0; c < 24; ++c) h += A.w0[r * 24 + c] * feat[c];
         h = h < 0.0f ? 0.0f : h;
-        for (int j = 0; j < M.W; ++j) out[j] += __ldg(W1 + j * 64 + r) * h;
+#pragma unroll
+        for (int j = 0; j < W; ++j) out[j] += A.w1[j * 64 + r] * h;
     }
 }
 
@@ -165,7 +188,8 @@ __device__ float decode_sigma_pre(const DevModel& M, const CornerTable& T, const
     }
     float fine[NGPRT_MAX_FINE_LEVELS][8];
     for (int l = 0; l < M.L; ++l)
-        interp<8>(M.fine[l], M.fine_res[l], M.fine_h[l], M.fine_len[l], M.fine_hashed[l], x, fine[l]);
+        interp<8>(M.fine[l], M.fine_res[l], M.fine_h[l], M.fine_len[l], M.fine_mask[l],
+                  M.fine_hashed[l], x, fine[l]);
     float out0 = dec[0];
     if (M.fusion == NGPRT_FUSION_MLP) {  // fusion.hpp:162-171, channel 0 of the output
         const int IN = 8 * M.L;
@@ -302,15 +326,31 @@ __global__ void corner_marks_kernel(const uint32_t* __restrict__ occ, int lc, ui
     }
 }
 
-// (3) evaluate_corner for every retained corner key.
-__global__ void corner_eval_kernel(const DevModel M, const unsigned long long* __restrict__ keys,
-                                   size_t n, float* __restrict__ rows) {
+// (3) evaluate_corner for every corner key.
+template <int W>
+__global__ void __launch_bounds__(128) corner_eval_kernel(const DevModel M,
+                                                          const __grid_constant__ AuxWeights A,
+                                                          const unsigned long long* __restrict__ keys,
+                                                          size_t n, float* __restrict__ rows) {
     const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const unsigned long long r1 = (unsigned long long)M.L_C + 1, key = keys[i];
-    float row[16];
-    evaluate_corner(M, int(key % r1), int((key / r1) % r1), int(key / (r1 * r1)), row);
-    for (int j = 0; j < M.W; ++j) rows[i * M.W + j] = row[j];
+    float row[W];
+    evaluate_corner<W>(M, A, int(key % r1), int((key / r1) % r1), int(key / (r1 * r1)), row);
+#pragma unroll
+    for (int j = 0; j < W; ++j) rows[i * W + j] = row[j];
+}
+
+void launch_corner_eval(const DevModel& M, const AuxWeights& A, const unsigned long long* keys,
+                        size_t n, float* rows) {
+    if (!n) return;
+    const unsigned g = unsigned((n + 127) / 128);
+    switch (M.W) {
+        case 10: corner_eval_kernel<10><<<g, 128>>>(M, A, keys, n, rows); break;
+        case 12: corner_eval_kernel<12><<<g, 128>>>(M, A, keys, n, rows); break;
+        case 14: corner_eval_kernel<14><<<g, 128>>>(M, A, keys, n, rows); break;
+        default: corner_eval_kernel<16><<<g, 128>>>(M, A, keys, n, rows); break;
+    }
 }
 
 // Retained corner keys in ascending order (== the reference's z,y,x scan,
@@ -573,21 +613,21 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
             M.ch[k] = float(res) / 2.0f;
             M.cdirect[k] = corners <= md->coarse_table_len;
             M.clen[k] = len;
+            M.cmask[k] = (!M.cdirect[k] && (len & (len - 1)) == 0) ? len - 1 : 0;
             M.ctab[k] = db.upload(md->coarse_tables[k], len * 4);
         }
-        {
-            std::vector<float> aux(64 * 24 + 64 + W * 64 + W);
-            std::memcpy(aux.data(), md->aux_w[0], 64 * 24 * 4);
-            std::memcpy(aux.data() + 64 * 24, md->aux_b[0], 64 * 4);
-            std::memcpy(aux.data() + 64 * 24 + 64, md->aux_w[1], size_t(W) * 64 * 4);
-            std::memcpy(aux.data() + 64 * 24 + 64 + W * 64, md->aux_b[1], size_t(W) * 4);
-            M.aux = db.upload(aux.data(), aux.size());
-        }
+        auto A = std::make_unique<AuxWeights>();
+        std::memset(A.get(), 0, sizeof(AuxWeights));
+        std::memcpy(A->w0, md->aux_w[0], 64 * 24 * 4);
+        std::memcpy(A->b0, md->aux_b[0], 64 * 4);
+        std::memcpy(A->w1, md->aux_w[1], size_t(W) * 64 * 4);
+        std::memcpy(A->b1, md->aux_b[1], size_t(W) * 4);
         for (int l = 0; l < L; ++l) {
             M.fine_res[l] = int(md->fine_res[l]);
             M.fine_h[l] = float(md->fine_res[l]) / 2.0f;
             M.fine_hashed[l] = md->fine_hashed[l];
             M.fine_len[l] = md->fine_table_len[l];
+            M.fine_mask[l] = (M.fine_hashed[l] && (M.fine_len[l] & (M.fine_len[l] - 1)) == 0) ? M.fine_len[l] - 1 : 0;
             M.fine[l] = db.upload(md->fine_tables[l], md->fine_table_len[l] * 8);
         }
         M.fusion = md->fusion_tag;
@@ -643,7 +683,7 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
             unsigned long long* ckeys;
             const uint32_t nc = compact(cmarks, nw, &coffsets, &ckeys);
             float* crows = db.alloc<float>(size_t(nc ? nc : 1) * W);
-            if (nc) corner_eval_kernel<<<blocks(nc, 128), 128>>>(M, ckeys, nc, crows);
+            launch_corner_eval(M, *A, ckeys, nc, crows);
             check_cuda("bake: cull corners");
             pt.mark("cull_corners");
             cull_table = CornerTable{cmarks, coffsets, crows, (unsigned long long)r1, W};
@@ -721,7 +761,7 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
         pt.mark("keys");
         if (n_keys) {
             float* drows = db.alloc<float>(b->rows.size());
-            corner_eval_kernel<<<blocks(n_keys, 128), 128>>>(M, dkeys, n_keys, drows);
+            launch_corner_eval(M, *A, dkeys, n_keys, drows);
             check_cuda("bake: corner evaluation");
             pt.mark("corner_kernel");
             d2h(b->keys.data(), dkeys, size_t(n_keys) * 8);
