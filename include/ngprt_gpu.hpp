@@ -6,6 +6,7 @@
 //     #include "ngprt_gpu.hpp"
 //     ngprt::gpu::Scene gs(baked);                  // upload once (ngprt_scene_create)
 //     ngprt::Image img = gs.render(dataset, frame); // == render_ray over every pixel
+//     ngprt::BakedScene b = ngprt::gpu::bake(model, train_grid, opts);  // == bake()
 //
 // Requires the reference headers (/root/reference/proj/include) on the include
 // path and links against paper_2407_10482_b200/_lib/libngprt_cuda.so.
@@ -13,6 +14,7 @@
 // reference's own exceptions.
 #pragma once
 
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -63,6 +65,11 @@ public:
         }
         d.fusion_tag = uint8_t(s.tag);
         d.att_globals = fusion_is_invariant(s.tag) ? s.fusion.global_pre.value.data() : nullptr;
+        if (s.tag == FusionTag::Mlp)
+            for (int k = 0; k < 2; ++k) {
+                d.fusion_mlp_w[k] = s.fusion.mlp.weight[k].value.data();
+                d.fusion_mlp_b[k] = s.fusion.mlp.bias[k].value.data();
+            }
         d.occ_base_res = uint32_t(s.pyramid.levels[0].res);
         for (int k = 0; k < kPyramidLevels; ++k) d.pyramid_words[k] = s.pyramid.levels[k].words.data();
         d.dist_res = uint32_t(s.distance.resolution);
@@ -119,6 +126,91 @@ private:
 inline Image render(const BakedScene& s, const PosedDataset& ds, size_t frame,
                     const RenderOptions& o = {}, int device = 0) {
     return Scene(s, device).render(ds, frame, o);
+}
+
+// bake (baking.hpp:107-202) on the GPU: the same model, training grid and
+// options in, the same BakedScene out (save_baked writes the reference's file
+// byte for byte; tests/test_bake.py, tests/cpp/adapter_demo.cpp).
+inline BakedScene bake(const NgpRtModel<float>& model, const BitGrid& train_grid,
+                       const BakeOptions& opt = {}, int device = 0) {
+    const int L = model.cfg.fine_levels, lc = model.corner_res(), w = model.decoder_width();
+    ngprt_model_desc d{};
+    d.L = uint32_t(L);
+    d.L_C = uint32_t(lc);
+    d.coarse_table_len = model.cfg.coarse_table_len;
+    for (int k = 0; k < kCoarseLevels; ++k) {
+        d.coarse_res[k] = uint32_t(model.encoding.coarse[k].resolution);
+        d.coarse_tables[k] = model.encoding.coarse[k].entries.value.data();
+    }
+    for (int k = 0; k < 2; ++k) {
+        d.aux_w[k] = model.aux.weight[k].value.data();
+        d.aux_b[k] = model.aux.bias[k].value.data();
+    }
+    for (int l = 0; l < L; ++l) {
+        const auto& f = model.encoding.fine[l];
+        d.fine_res[l] = uint32_t(f.resolution);
+        d.fine_table_len[l] = f.table_len;
+        d.fine_hashed[l] = f.addressing == Addressing::Hashed ? 1 : 0;
+        d.fine_tables[l] = f.entries.value.data();
+    }
+    for (int k = 0; k < 3; ++k) {
+        d.psi_w[k] = model.psi.weight[k].value.data();
+        d.psi_b[k] = model.psi.bias[k].value.data();
+    }
+    d.fusion_tag = uint8_t(model.fusion_tag);
+    if (fusion_is_invariant(model.fusion_tag)) d.att_globals = model.fusion.global_pre.value.data();
+    if (model.fusion_tag == FusionTag::Mlp)
+        for (int k = 0; k < 2; ++k) {
+            d.fusion_mlp_w[k] = model.fusion.mlp.weight[k].value.data();
+            d.fusion_mlp_b[k] = model.fusion.mlp.bias[k].value.data();
+        }
+    const ngprt_bake_opts o{opt.cull_step, opt.cull_alpha_thresh, uint32_t(opt.dilate_voxels), 0};
+    ngprt_baked* raw = nullptr;
+    check(ngprt_bake(&d, train_grid.words.data(), uint32_t(train_grid.res), &o, device, &raw),
+          "ngprt_bake");
+    std::unique_ptr<ngprt_baked, void (*)(ngprt_baked*)> b(raw, ngprt_baked_free);
+    const ngprt_scene_desc& r = *ngprt_baked_desc(b.get());
+
+    BakedScene out;  // assembled as bake() does (baking.hpp:114-116, 137-200)
+    out.cfg = model.cfg;
+    out.tag = model.fusion_tag;
+    out.coarse.init(lc, L);
+    out.coarse.rows.assign(r.coarse_rows, r.coarse_rows + r.n_coarse * size_t(w));
+    out.coarse.index.reserve(r.n_coarse);
+    for (uint64_t i = 0; i < r.n_coarse; ++i) out.coarse.index.emplace(r.coarse_keys[i], uint32_t(i));
+    out.fine.resize(L);
+    for (int l = 0; l < L; ++l) {
+        const auto& f = model.encoding.fine[l];
+        out.fine[l].resolution = f.resolution;
+        out.fine[l].table_len = f.table_len;
+        out.fine[l].feature_dim = f.feature_dim;
+        out.fine[l].addressing = f.addressing;
+        out.fine[l].entries.init("fine_l" + std::to_string(l + 1), f.entries.size(), false);
+        out.fine[l].entries.value = f.entries.value;
+    }
+    Rng dummy(0);
+    out.psi.init({kShadeInWidth, 64, 64, 3}, "psi", dummy, nullptr);
+    for (int k = 0; k < out.psi.num_layers(); ++k) {
+        out.psi.weight[k].value = model.psi.weight[k].value;
+        out.psi.bias[k].value = model.psi.bias[k].value;
+    }
+    out.fusion.init(model.fusion_tag, L, dummy, nullptr);
+    if (fusion_is_invariant(model.fusion_tag)) out.fusion.global_pre.value = model.fusion.global_pre.value;
+    if (model.fusion_tag == FusionTag::Mlp)
+        for (int k = 0; k < out.fusion.mlp.num_layers(); ++k) {
+            out.fusion.mlp.weight[k].value = model.fusion.mlp.weight[k].value;
+            out.fusion.mlp.bias[k].value = model.fusion.mlp.bias[k].value;
+        }
+    for (int k = 0; k < kPyramidLevels; ++k) {
+        out.pyramid.levels[k] = BitGrid(int(r.occ_base_res) >> k);
+        std::copy(r.pyramid_words[k], r.pyramid_words[k] + out.pyramid.levels[k].words.size(),
+                  out.pyramid.levels[k].words.begin());
+    }
+    out.distance.resolution = int(r.dist_res);
+    out.distance.voxel_size = Roi::extent / r.dist_res;
+    out.distance.values.assign(r.dist_values,
+                               r.dist_values + size_t(r.dist_res) * r.dist_res * r.dist_res);
+    return out;
 }
 
 }  // namespace ngprt::gpu

@@ -5,11 +5,16 @@
 // FusionMode), renders it (a) with the reference's render path composed on the
 // CPU exactly as SURVEY.md §8(c) and (b) on the B200 through include/ngprt_gpu.hpp,
 // and compares with the reference's own max_abs_diff / psnr (image.hpp:89-110).
+// Then bakes a reference NgpRtModel (model.hpp:27-107) with the reference's
+// bake() and with ngprt::gpu::bake() and compares the two save_baked files.
 // Feature values are NOT fp16-representable, so the GPU picks f32 storage.
 // Prints one JSON line; tests/test_gpu_adapter.py checks it.
 #include "ngprt_gpu.hpp"
 
 #include <cstdio>
+#include <fstream>
+#include <iterator>
+#include <unistd.h>
 
 using namespace ngprt;
 
@@ -85,6 +90,37 @@ static Image cpu_render(const BakedScene& s, const PosedDataset& ds, size_t f,
     return img;
 }
 
+static std::string slurp(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    return std::string(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+}
+
+// Reference model in the "desk" geometry (config.hpp:60-68) with non-trivial
+// parameters, its training grid, both bakes, byte comparison of the files.
+static bool bake_identical(size_t* corners) {
+    RunConfig rc = RunConfig::desk();
+    NgpRtModel<float> m;
+    m.init(rc.enc, FusionTag::SeparateAttV, 7);
+    Rng rng(99);
+    for (auto& lvl : m.encoding.coarse)
+        for (auto& v : lvl.entries.value) v = float(rng.uniform(-1.0, 1.0));
+    for (auto& lvl : m.encoding.fine)
+        for (auto& v : lvl.entries.value) v = float(rng.uniform(-0.5, 0.5));
+    m.aux.bias[1].value[0] = -0.5f;  // density offset: the cull keeps about half the voxels
+    const BitGrid grid = scene_occupancy(make_scene("toy"), rc.train_grid_res);
+    const BakedScene rb = bake(m, grid);
+    const BakedScene gb = gpu::bake(m, grid);
+    const std::string pa = "/tmp/adapter_demo_ref_" + std::to_string(getpid()) + ".ngrt";
+    const std::string pb = "/tmp/adapter_demo_gpu_" + std::to_string(getpid()) + ".ngrt";
+    save_baked(rb, pa);
+    save_baked(gb, pb);
+    const bool same = slurp(pa) == slurp(pb) && !slurp(pa).empty();
+    std::remove(pa.c_str());
+    std::remove(pb.c_str());
+    *corners = gb.coarse.count();
+    return same;
+}
+
 int main() {
     const BakedScene s = make_baked(2024);
     PosedDataset ds;
@@ -115,9 +151,12 @@ int main() {
     }
     ngprt_scene_info info{};
     ngprt_scene_info_get(gs.handle(), &info);
+    size_t bake_corners = 0;
+    const bool bake_same = bake_identical(&bake_corners);
     std::printf("{\"frames\": %zu, \"max_abs_exact\": %.9g, \"max_abs_tensor\": %.9g, "
-                "\"psnr_tensor\": %.3f, \"counter_mismatch\": %ld, \"storage\": %d}\n",
+                "\"psnr_tensor\": %.3f, \"counter_mismatch\": %ld, \"storage\": %d, "
+                "\"bake_identical\": %s, \"bake_corners\": %zu}\n",
                 ds.frames.size(), worst_exact, worst_tc, min_psnr_tc, counter_mismatch,
-                int(info.storage));
+                int(info.storage), bake_same ? "true" : "false", bake_corners);
     return 0;
 }

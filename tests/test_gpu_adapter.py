@@ -28,3 +28,6 @@ def test_adapter_renders_reference_baked_scene():
     assert r["max_abs_tensor"] <= 1e-3        # north_star RGB tolerance
     assert r["psnr_tensor"] >= 60.0
     assert r["storage"] == 1                  # non-fp16-exact values -> f32 storage
+    # ngprt::gpu::bake over a reference NgpRtModel == the reference's bake(), file for file
+    assert r["bake_identical"] is True
+    assert r["bake_corners"] > 0
