@@ -43,6 +43,10 @@ namespace ngprt_dev {
 namespace {
 
 constexpr int kCoarseLevels = 6;
+constexpr int kHiddenUnroll = 64;
+#ifndef NGPRT_CORNER_MINB
+#define NGPRT_CORNER_MINB 10
+#endif
 
 struct DevModel {
     int L, L_C, W;  // W = 8 + 2L
@@ -141,7 +145,9 @@ __device__ __forceinline__ void evaluate_corner(const DevModel& M, const AuxWeig
     // accumulates in the same c-order as the reference's inner loop.
 #pragma unroll
     for (int j = 0; j < W; ++j) out[j] = A.b1[j];
-#pragma unroll
+    // r unrolled by kHiddenUnroll only: a full unroll (~8 k instructions)
+    // overflows the instruction cache (ncu: "no instructions" top stall).
+#pragma unroll kHiddenUnroll
     for (int r = 0; r < 64; ++r) {
         float h = A.b0[r];
 #pragma unroll
@@ -328,7 +334,7 @@ __global__ void corner_marks_kernel(const uint32_t* __restrict__ occ, int lc, ui
 
 // (3) evaluate_corner for every corner key.
 template <int W>
-__global__ void __launch_bounds__(128) corner_eval_kernel(const DevModel M,
+__global__ void __launch_bounds__(128, NGPRT_CORNER_MINB) corner_eval_kernel(const DevModel M,
                                                           const __grid_constant__ AuxWeights A,
                                                           const unsigned long long* __restrict__ keys,
                                                           size_t n, float* __restrict__ rows) {
