@@ -633,23 +633,21 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
         s.n_occ_acc += uint32_t(e) + 1u;
         exit_k = 4 - e;
     }
-    // next_step (occupancy.hpp:261-276) on the unclamped point ray.at(t)
-    int iu[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) iu[a] = (xu[a] == s.xc[a]) ? i0[a] : voxel_1d(xu[a], sc.occ_h0, r0);
+    // next_step (occupancy.hpp:261-276) on the unclamped point ray.at(t). Its
+    // voxel_of clamps the index to [0, res-1], so the unclamped point's voxel is
+    // the clamped point's: (x+1)*h < 0 <=> x < -1 and (x+1)*h >= res <=> x >= 1.
+    const int* iu = i0;
     const int res = sc.occ_res[exit_k];
     uint32_t g = 0;
     const bool consult = p.use_grid && sc.dist && res < sc.dist_res;
     if (consult) {
         ++s.n_dist;
         if (sc.dist_is_l1) {
-            const int vx = iu[0] >> 1, vy = iu[1] >> 1, vz = iu[2] >> 1;
-            const uint32_t di = uint32_t(vx) + uint32_t(r1) * (uint32_t(vy) + uint32_t(r1) * uint32_t(vz));
-            g = (di == pidx) ? (code & 0xffu) : uint32_t(__ldg(sc.dist + di));
+            g = code & 0xffu;  // the probe code's own level-1 voxel (iu >> 1 == pidx's voxel)
         } else {
             const int gr = sc.dist_res;
-            const int vx = voxel_1d(xu[0], sc.dist_h, gr), vy = voxel_1d(xu[1], sc.dist_h, gr),
-                      vz = voxel_1d(xu[2], sc.dist_h, gr);
+            const int vx = voxel_1d(s.xc[0], sc.dist_h, gr), vy = voxel_1d(s.xc[1], sc.dist_h, gr),
+                      vz = voxel_1d(s.xc[2], sc.dist_h, gr);
             g = __ldg(sc.dist + (size_t(vx) + size_t(gr) * (size_t(vy) + size_t(gr) * vz)));
         }
     }
@@ -659,19 +657,46 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
         // and no side effect, so voxel_exit_step is skipped (same t sequence).
         step = sc.dist_vox * float(g);
     } else {
-        // voxel_exit_step (occupancy.hpp:238-255)
-        float t_exit = 3.402823466e38f;
+        // voxel_exit_step (occupancy.hpp:238-255): t_exit = min over axes of the
+        // IEEE quotient (bound - o) / d. RN division is monotonic, so the min is the
+        // quotient of the axis with the smallest exact ratio: an approximate ratio
+        // (MUFU.RCP, a few ulp) picks it and one exact division evaluates it. Axes
+        // within 2^-16 relative of the approximate minimum (near-ties, or anything
+        // non-finite) are all evaluated exactly; the result is the reference's.
+        float num[3], q[3];
+        float qmin = 3.402823466e38f;
+        int amin = -1;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const float d = s.ray.d[a];
-            if (d == 0.0f) continue;
             const float v2 = 2.0f * float(iu[a] >> exit_k);
             // T(extent)*T(v)/T(res): a power-of-two divisor is an exact reciprocal multiply
             const float lo = -1.0f + (sc.occ_pow2 ? v2 * sc.lvl_inv_res[exit_k] : v2 / float(res));
             const float hi = lo + sc.lvl_two_over_res[exit_k];
-            const float bound = d > 0.0f ? hi : lo;
-            const float tc = (bound - s.ray.o[a]) / d;
+            num[a] = (d > 0.0f ? hi : lo) - s.ray.o[a];
+            float rd;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d));
+            q[a] = (d == 0.0f) ? 3.402823466e38f : num[a] * rd;
+            if (d != 0.0f && !(q[a] >= qmin)) {  // NaN-safe argmin
+                qmin = q[a];
+                amin = a;
+            }
+        }
+        float t_exit = 3.402823466e38f;
+        if (amin >= 0) {
+            const float dsel = amin == 0 ? s.ray.d[0] : (amin == 1 ? s.ray.d[1] : s.ray.d[2]);
+            const float nsel = amin == 0 ? num[0] : (amin == 1 ? num[1] : num[2]);
+            const float tc = nsel / dsel;
             t_exit = (tc < t_exit) ? tc : t_exit;
+            const float margin = fabsf(qmin) * 1.52587890625e-5f + 1e-30f;  // 2^-16
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (a == amin || s.ray.d[a] == 0.0f) continue;
+                if (!(q[a] > qmin + margin) || !(fabsf(q[a]) < 3.0e38f)) {  // near-tie: exact too
+                    const float tc2 = num[a] / s.ray.d[a];
+                    t_exit = (tc2 < t_exit) ? tc2 : t_exit;
+                }
+            }
         }
         float sz = t_exit - s.t;
         if (!(sz > 0.0f)) sz = 0.0f;
