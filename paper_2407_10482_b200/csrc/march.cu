@@ -195,6 +195,22 @@ __device__ __forceinline__ unsigned long long fine_index(const DevScene& sc, int
     return (unsigned long long)x + r1 * ((unsigned long long)y + r1 * (unsigned long long)z);
 }
 
+// Multiply-accumulate of one channel: exact (separate f32 multiply and add,
+// the reference's -ffp-contract=off rounding) or, for the colour channels in
+// tensor-MLP mode (FC), one FMA. Channels that feed density, attention
+// weights or transmittance are always exact, so marching, early stop and the
+// per-ray counters are bit-identical in both modes.
+// (`fma` is a compile-time constant at every call site after unrolling.)
+__device__ __forceinline__ float mac(bool fma, float acc, float w, float v) {
+    return fma ? __fmaf_rn(w, v, acc) : acc + w * v;
+}
+
+// Coarse decoder channels that must stay exact: sigma_pre (0) and the omega
+// logits (8 + 2l), which set the density fuse weights of the variant modes.
+__device__ __forceinline__ constexpr bool exact_channel(int c) {
+    return c == 0 || (c >= 8 && ((c - 8) & 1) == 0);
+}
+
 // Trilinear weights in corner order k (bit0 x, bit1 y, bit2 z): w_k = (wx*wy)*wz
 // (hash_grid.hpp:50-54); the wx*wy products are shared, the values are identical.
 __device__ __forceinline__ void corner_weights(const float f[3], float w[8]) {
@@ -210,7 +226,7 @@ __device__ __forceinline__ void corner_weights(const float f[3], float w[8]) {
 // Interpolate fine level l at x (hash_grid.hpp:97-106: out[c] = sum_k w_k row_k[c],
 // corner order k = 0..7 from a zero start). Power-of-two hashed tables take the
 // unrolled path; direct / generic-length levels a compact loop (rare).
-template <bool F16>
+template <bool F16, bool FC = false>
 __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const float x[3],
                                            float fine[8]) {
     int b[3];
@@ -236,7 +252,7 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
 #pragma unroll
         for (int k = 0; k < 8; ++k)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) fine[c] += w[k] * frow[k][c];
+            for (int c = 0; c < 8; ++c) fine[c] = mac(FC && c != 0, fine[c], w[k], frow[k][c]);
     } else {
 #pragma unroll 1
         for (int k = 0; k < 8; ++k) {
@@ -246,7 +262,7 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
             float row[8];
             load_fine_row<F16>(table, fine_index(sc, l, b[0] + dx, b[1] + dy, b[2] + dz), row);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) fine[c] += wk * row[c];
+            for (int c = 0; c < 8; ++c) fine[c] = mac(FC && c != 0, fine[c], wk, row[c]);
         }
     }
 }
@@ -407,13 +423,17 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
 #ifndef NGPRT_FINE_PREFETCH
 #define NGPRT_FINE_PREFETCH 1
 #endif
-template <int L>
+template <int L, bool FC>
 __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const float x[3],
                                                   int keep_level, const unsigned long long* tab,
                                                   float* scr, float out[8]) {
     constexpr int W = 8 + 2 * L;
     constexpr int P = NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L;
-    constexpr int CW = W <= 12 ? 6 : 8;  // u32 words of a coarse row actually needed
+#ifndef NGPRT_COARSE_FULL_ROW
+#define NGPRT_COARSE_FULL_ROW 0
+#endif
+    // u32 words of a coarse row actually loaded (W <= 12: 128+64-bit loads, else one 256-bit)
+    constexpr int CW = (W <= 12 && !NGPRT_COARSE_FULL_ROW) ? 6 : 8;
     // ---- issue: coarse rows ----
     int cb[3];
     float cf[3];
@@ -466,8 +486,8 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
             for (int i = 0; i < W / 2; ++i) {
                 const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&craw[k][i]));
-                dec[2 * i] += w[k] * v.x;
-                dec[2 * i + 1] += w[k] * v.y;
+                dec[2 * i] = mac(FC && !exact_channel(2 * i), dec[2 * i], w[k], v.x);
+                dec[2 * i + 1] = mac(FC && !exact_channel(2 * i + 1), dec[2 * i + 1], w[k], v.y);
             }
     }
     // ---- attention (split_decoder_output, model.hpp:18-21) ----
@@ -514,8 +534,8 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float2 v = __half22float2(h[i]);
-                fine[2 * i] += w[k] * v.x;
-                fine[2 * i + 1] += w[k] * v.y;
+                fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
+                fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
             }
         }
         if (keep_level > 0 && l + 1 != keep_level) {
@@ -526,13 +546,13 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         weights(l, wo, wb);
         out[0] += wo * fine[0];
 #pragma unroll
-        for (int c = 1; c < 8; ++c) out[c] += wb * fine[c];
+        for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
     }
     // ---- remaining levels one round trip each ----
 #pragma unroll 1
     for (int l = P; l < L; ++l) {
         float fine[8];
-        fine_level<true>(sc, l, x, fine);
+        fine_level<true, FC>(sc, l, x, fine);
         if (keep_level > 0 && l + 1 != keep_level) {
 #pragma unroll
             for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
@@ -541,7 +561,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         weights(l, wo, wb);
         out[0] += wo * fine[0];
 #pragma unroll
-        for (int c = 1; c < 8; ++c) out[c] += wb * fine[c];
+        for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
     }
 }
 
@@ -597,6 +617,22 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
     s.has_ray = true;
 }
 
+// Probe-code layout: 4x4x4 bricks of level-1 voxels (128 B = one L1 line,
+// 4x4x1 per 32 B sector), bricks x-fastest. Lanes of a warp sit at different
+// depths of neighbouring rays and a lane's successive points move in any
+// direction, so a brick keeps more of them in one line than x-major rows do.
+#ifndef NGPRT_PROBE_BRICK
+#define NGPRT_PROBE_BRICK 1
+#endif
+__device__ __forceinline__ uint32_t probe_index(uint32_t x, uint32_t y, uint32_t z, uint32_t r1) {
+#if NGPRT_PROBE_BRICK
+    const uint32_t rb = r1 >> 2;
+    return (((x >> 2) + rb * ((y >> 2) + rb * (z >> 2))) << 6) | ((z & 3u) << 4) | ((y & 3u) << 2) | (x & 3u);
+#else
+    return x + r1 * (y + r1 * z);
+#endif
+}
+
 // One marching point (march, occupancy.hpp:310-324): probe (:218-231) via the
 // per-level-1 probe code; occupied -> park for decode; empty -> next_step (:261-276).
 // Returns false when the ray left the clip interval.
@@ -614,8 +650,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
 #pragma unroll
     for (int a = 0; a < 3; ++a) i0[a] = voxel_1d(s.xc[a], sc.occ_h0, r0);
     // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
-    const uint32_t pidx =
-        uint32_t(i0[0] >> 1) + uint32_t(r1) * (uint32_t(i0[1] >> 1) + uint32_t(r1) * uint32_t(i0[2] >> 1));
+    const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
     const uint32_t code = __ldg(sc.probe + pidx);
     const int e = int(code >> 8) & 7;
     int exit_k;
@@ -711,7 +746,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     return true;
 }
 
-template <int L, bool F16, bool MLPF>
+template <int L, bool F16, bool MLPF, bool FC>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScene sc,
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
@@ -765,7 +800,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
                 float f[8];
                 if constexpr (F16 && !MLPF) {
                     if (sc.fast_decode)
-                        decode_point_fast<L>(sc, s.xc, p.keep_level, tab, scr, f);
+                        decode_point_fast<L, FC>(sc, s.xc, p.keep_level, tab, scr, f);
                     else
                         decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
                 } else {
@@ -776,9 +811,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
                 const float a = alpha_from_sigma(sigma, step, tab);
                 const float w = a * s.T;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) s.cd[c] += w * f[1 + c];
+                for (int c = 0; c < 3; ++c) s.cd[c] = mac(FC, s.cd[c], w, f[1 + c]);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) s.fs[c] += w * f[4 + c];
+                for (int c = 0; c < 4; ++c) s.fs[c] = mac(FC, s.fs[c], w, f[4 + c]);
                 s.T = s.T * (1.0f - a);
                 s.pending = false;
                 if (p.early_stop && s.T < float(2e-3)) {  // kEarlyStopTransmittance
@@ -831,26 +866,26 @@ __global__ void __launch_bounds__(256) raygen_kernel(const MarchParams p) {
     if (p.stats) p.stats[idx] = ngprt_ray_stats{0u, 0u, 0u, 0u};
 }
 
-template <int L, bool F16, bool MLPF>
+template <int L, bool F16, bool MLPF, bool FC = false>
 int ctas_per_sm_t() {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<L, F16, MLPF>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<L, F16, MLPF, FC>, kBlock, 0);
     return n > 0 ? n : 1;
 }
 
-template <int L, bool F16, bool MLPF>
+template <int L, bool F16, bool MLPF, bool FC = false>
 void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
     static int grid = 0;
     if (!grid) {
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = sms * ctas_per_sm_t<L, F16, MLPF>();
+        grid = sms * ctas_per_sm_t<L, F16, MLPF, FC>();
     }
     raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
     const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);
     const uint32_t need = (tiles + 3) / 4;  // 4 warps per CTA
-    march_kernel<L, F16, MLPF><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
+    march_kernel<L, F16, MLPF, FC><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
 }
 
 template <int L>
@@ -859,7 +894,10 @@ void launch_l(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
     if (mlp) {
         f16 ? launch_t<L, true, true>(sc, p, st) : launch_t<L, false, true>(sc, p, st);
     } else {
-        f16 ? launch_t<L, true, false>(sc, p, st) : launch_t<L, false, false>(sc, p, st);
+        if (f16 && sc.fast_decode && p.fast_color)
+            launch_t<L, true, false, true>(sc, p, st);
+        else
+            f16 ? launch_t<L, true, false>(sc, p, st) : launch_t<L, false, false>(sc, p, st);
     }
 }
 
@@ -895,7 +933,7 @@ __global__ void probe_code_kernel(const DevScene sc, uint16_t* __restrict__ out)
         } else {
             payload = (sc.dist && sc.dist_is_l1) ? sc.dist[i] : 0u;
         }
-        out[i] = uint16_t((e << 8) | payload);
+        out[probe_index(uint32_t(x), uint32_t(y), uint32_t(z), uint32_t(r1))] = uint16_t((e << 8) | payload);
     }
 }
 

@@ -496,6 +496,14 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         }();
         p.decode_min = dmin;
         p.step_burst = burst;
+        // Tensor-MLP mode tolerates 1e-3 on RGB: K1 then accumulates the colour
+        // channels with FMA (density / attention / transmittance stay exact, so
+        // the per-ray counters do too). NGPRT_FAST_COLOR=0 keeps them exact.
+        static const int fast_color = [] {
+            const char* e = std::getenv("NGPRT_FAST_COLOR");
+            return e ? (std::atoi(e) != 0) : 1;
+        }();
+        p.fast_color = (o->mlp_mode == NGPRT_MLP_TENSOR) && fast_color;
     }
     p.tiles_x = (W + 7) / 8;
     p.tiles_per_cam = p.tiles_x * ((H + 3) / 4);

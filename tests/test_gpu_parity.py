@@ -212,6 +212,13 @@ def test_full_1080p_frame_matches_oracle(ng, torch):
     want_rgb, want_stats = o.render(cam, opts.to_c())
     assert np.array_equal(stats, want_stats)
     assert np.array_equal(rgb.view(np.uint32), want_rgb.view(np.uint32))
+    # the bench mode (tensor MLP, FMA colour accumulation in K1): counters still
+    # bit-exact on every ray, RGB within the north_star tolerance
+    t_rgb, t_stats = gpu_render(ng, torch, dev, cam, ng.Opts(mlp="tensor"))
+    assert np.array_equal(t_stats, want_stats)
+    assert np.array_equal(t_rgb.sum(-1) == 0, want_rgb.sum(-1) == 0)
+    assert np.abs(t_rgb - want_rgb).max() <= RGB_TOL
+    assert psnr(t_rgb, want_rgb) >= PSNR_MIN
 
 
 def test_multi_camera_batch_and_window_consistency(ng, torch):
