@@ -160,6 +160,19 @@ ngprt_status ngprt_render_host(const ngprt_scene* scene, const ngprt_camera* cam
                                const ngprt_render_opts* opts, float* rgb_host,
                                ngprt_ray_stats* stats_host);
 
+/* Pipelined host-buffer rendering for a stream of frames (serving). Same
+ * arguments as ngprt_render_host, but returns once the frame is enqueued: it is
+ * rendered into a device buffer and copied to rgb_host / stats_host by the copy
+ * engine while the NEXT enqueued frame renders, so the device->host transfer
+ * overlaps the march. At most two frames are in flight per scene (enqueueing a
+ * third waits for the oldest). Host buffers must stay valid, and should be
+ * pinned for the copy to be asynchronous, until ngprt_render_host_wait returns. */
+ngprt_status ngprt_render_host_async(const ngprt_scene* scene, const ngprt_camera* cams,
+                                     int n_cams, const ngprt_render_opts* opts, float* rgb_host,
+                                     ngprt_ray_stats* stats_host);
+/* Blocks until every frame enqueued with ngprt_render_host_async is in host memory. */
+ngprt_status ngprt_render_host_wait(const ngprt_scene* scene);
+
 /* Per-kernel device time of the most recent ngprt_render on this scene with
  * opts.profile set: CUDA events recorded on the render stream around the march
  * kernel (K1) and the deferred-MLP kernel (K2), summed over launches. Call

@@ -168,6 +168,9 @@ SIGNATURES = {
                                C.c_void_p, C.c_void_p, C.c_void_p]),
     "ngprt_render_host": (C.c_int, [C.c_void_p, C.POINTER(Camera), C.c_int, C.POINTER(RenderOpts),
                                     C.c_void_p, C.c_void_p]),
+    "ngprt_render_host_async": (C.c_int, [C.c_void_p, C.POINTER(Camera), C.c_int,
+                                          C.POINTER(RenderOpts), C.c_void_p, C.c_void_p]),
+    "ngprt_render_host_wait": (C.c_int, [C.c_void_p]),
     "ngprt_render_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                       C.POINTER(C.c_int)]),
     "ngprt_build_pyramid": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p * (PYRAMID_LEVELS - 1),

@@ -72,6 +72,22 @@ struct ngprt_scene {
         std::vector<cudaEvent_t> band_done;
     };
     mutable HostCtx host;
+    // ngprt_render_host_async: two frame slots (device outputs + completion
+    // events), one render stream, one copy stream.
+    struct AsyncCtx {
+        std::mutex mu;
+        cudaStream_t render = nullptr, copy = nullptr;
+        struct Slot {
+            float* rgb = nullptr;
+            size_t rgb_cap = 0;
+            ngprt_ray_stats* stats = nullptr;
+            size_t stats_cap = 0;
+            cudaEvent_t rendered = nullptr, copied = nullptr;
+            bool busy = false;
+        } slot[2];
+        int next = 0;
+    };
+    mutable AsyncCtx async;
 
     ~ngprt_scene() {
         int prev = 0;
@@ -84,6 +100,16 @@ struct ngprt_scene {
         if (host.copy) cudaStreamDestroy(host.copy);
         if (host.rgb) cudaFree(host.rgb);
         if (host.stats) cudaFree(host.stats);
+        if (async.render) cudaStreamSynchronize(async.render);
+        if (async.copy) cudaStreamSynchronize(async.copy);
+        for (auto& sl : async.slot) {
+            if (sl.rgb) cudaFree(sl.rgb);
+            if (sl.stats) cudaFree(sl.stats);
+            if (sl.rendered) cudaEventDestroy(sl.rendered);
+            if (sl.copied) cudaEventDestroy(sl.copied);
+        }
+        if (async.render) cudaStreamDestroy(async.render);
+        if (async.copy) cudaStreamDestroy(async.copy);
         for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
         cudaSetDevice(prev);
@@ -659,6 +685,73 @@ ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, i
         status = fail(NGPRT_ECUDA, std::string("ngprt_render_host: ") +
                                        cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
     return status;
+}
+
+ngprt_status ngprt_render_host_async(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
+                                     const ngprt_render_opts* o, float* rgb_host,
+                                     ngprt_ray_stats* stats_host) {
+    if (!s || !cams || !o || !rgb_host)
+        return fail(NGPRT_EINVAL, "ngprt_render_host_async: null argument");
+    if (n_cams <= 0) return fail(NGPRT_EINVAL, "ngprt_render_host_async: n_cams must be > 0");
+    NG_CUDA(cudaSetDevice(s->device));
+    const bool window = o->w && o->h;
+    const uint32_t W = window ? o->w : cams[0].width, H = window ? o->h : cams[0].height;
+    const size_t n = size_t(W) * H * size_t(n_cams);
+    std::lock_guard<std::mutex> lock(s->async.mu);
+    auto& ac = s->async;
+    if (!ac.render) {
+        NG_CUDA(cudaStreamCreateWithFlags(&ac.render, cudaStreamNonBlocking));
+        NG_CUDA(cudaStreamCreateWithFlags(&ac.copy, cudaStreamNonBlocking));
+        for (auto& sl : ac.slot) {
+            NG_CUDA(cudaEventCreateWithFlags(&sl.rendered, cudaEventDisableTiming));
+            NG_CUDA(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
+        }
+    }
+    auto& sl = ac.slot[ac.next];
+    ac.next ^= 1;
+    if (sl.busy) {  // the frame two back still owns this slot's device buffers
+        NG_CUDA(cudaEventSynchronize(sl.copied));
+        sl.busy = false;
+    }
+    if (sl.rgb_cap < n) {
+        if (sl.rgb) cudaFree(sl.rgb);
+        sl.rgb = nullptr;
+        NG_CUDA(cudaMalloc(&sl.rgb, n * 12));
+        sl.rgb_cap = n;
+    }
+    if (stats_host && sl.stats_cap < n) {
+        if (sl.stats) cudaFree(sl.stats);
+        sl.stats = nullptr;
+        NG_CUDA(cudaMalloc(&sl.stats, n * sizeof(ngprt_ray_stats)));
+        sl.stats_cap = n;
+    }
+    const ngprt_status st = render_impl(s, cams, n_cams, o, sl.rgb, stats_host ? sl.stats : nullptr,
+                                        ac.render);
+    if (st != NGPRT_OK) return st;
+    NG_CUDA(cudaEventRecord(sl.rendered, ac.render));
+    NG_CUDA(cudaStreamWaitEvent(ac.copy, sl.rendered, 0));
+    NG_CUDA(cudaMemcpyAsync(rgb_host, sl.rgb, n * 12, cudaMemcpyDeviceToHost, ac.copy));
+    if (stats_host)
+        NG_CUDA(cudaMemcpyAsync(stats_host, sl.stats, n * sizeof(ngprt_ray_stats),
+                                cudaMemcpyDeviceToHost, ac.copy));
+    NG_CUDA(cudaEventRecord(sl.copied, ac.copy));
+    sl.busy = true;
+    return NGPRT_OK;
+}
+
+ngprt_status ngprt_render_host_wait(const ngprt_scene* s) {
+    if (!s) return fail(NGPRT_EINVAL, "ngprt_render_host_wait: null scene");
+    std::lock_guard<std::mutex> lock(s->async.mu);
+    auto& ac = s->async;
+    if (!ac.render) return NGPRT_OK;
+    NG_CUDA(cudaSetDevice(s->device));
+    const cudaError_t e1 = cudaStreamSynchronize(ac.render);
+    const cudaError_t e2 = cudaStreamSynchronize(ac.copy);
+    for (auto& sl : ac.slot) sl.busy = false;
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+        return fail(NGPRT_ECUDA, std::string("ngprt_render_host_wait: ") +
+                                     cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    return NGPRT_OK;
 }
 
 ngprt_status ngprt_render_timing(const ngprt_scene* s, float* ms_march, float* ms_shade,

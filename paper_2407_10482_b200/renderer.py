@@ -365,6 +365,23 @@ def render_host(scene: Scene, cams, opts: Opts | None = None, out=None, stats=No
     return out
 
 
+def render_host_async(scene: Scene, cams, out, opts: Opts | None = None, stats=None):
+    """Enqueue a host-buffer render (ngprt_render_host_async) and return at once;
+    `out` (and `stats`) must stay alive, ideally pinned, until render_host_wait."""
+    opts = opts or Opts()
+    cams = camera_array(cams)
+    o = opts.to_c()
+    check(lib().ngprt_render_host_async(scene.handle, cams, len(cams), C.byref(o), out.ctypes.data,
+                                        stats.ctypes.data if stats is not None else None),
+          "ngprt_render_host_async")
+    return out
+
+
+def render_host_wait(scene: Scene) -> None:
+    """Block until every enqueued host-buffer frame is in host memory."""
+    check(lib().ngprt_render_host_wait(scene.handle), "ngprt_render_host_wait")
+
+
 def build_pyramid(base_words, base_res: int, stream=None):
     """Levels 1..4 of build_pyramid for a device u64 word tensor (torch.int64)."""
     import torch

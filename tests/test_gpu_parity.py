@@ -248,6 +248,28 @@ def test_render_host_matches_device_render(ng, torch):
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
+def test_render_host_async_pipeline_matches_sync(ng, torch):
+    """ngprt_render_host_async: five frames through two slots (the third and
+    later enqueues wait for a slot), pinned and pageable outputs, stats too;
+    every frame equals the synchronous ngprt_render_host result."""
+    scene = ng.SynthScene(occupancy="toy", occ_base_res=64, L=2, L_C=64, fine_table_len=1 << 12)
+    dev = ng.Scene(scene)
+    cams = ng.cameras(5, 40, 24)
+    opts = ng.Opts(mlp="tensor")
+    want = [ng.render_host(dev, [c], opts) for c in cams]
+    outs = [torch.empty((1, 24, 40, 3), dtype=torch.float32).pin_memory().numpy() if i % 2 == 0
+            else np.empty((1, 24, 40, 3), np.float32) for i in range(5)]
+    stats = [np.empty((1, 24, 40, 4), np.uint32) for _ in range(5)]
+    for c, o, st in zip(cams, outs, stats):
+        ng.render_host_async(dev, [c], o, opts, stats=st)
+    ng.render_host_wait(dev)
+    for i in range(5):
+        assert np.array_equal(outs[i].view(np.uint32), want[i].view(np.uint32)), i
+        want_st = np.empty((1, 24, 40, 4), np.uint32)
+        ng.render_host(dev, [cams[i]], opts, stats=want_st)
+        assert np.array_equal(stats[i], want_st), i
+
+
 def test_errors_are_reported(ng, torch):
     scene = ng.SynthScene(occupancy="slab", occ_base_res=64, L=2, L_C=32, fine_table_len=1 << 10)
     dev = ng.Scene(scene)
