@@ -653,21 +653,17 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
     const uint32_t code = __ldg(sc.probe + pidx);
     const int e = int(code >> 8) & 7;
-    int exit_k;
-    if (e == 4) {
-        s.n_occ_acc += 5;
-        // level-0 bit from the code's child byte (no second dependent load)
-        const uint32_t child = uint32_t(i0[0] & 1) | (uint32_t(i0[1] & 1) << 1) | (uint32_t(i0[2] & 1) << 2);
-        if ((code >> child) & 1u) {
-            ++s.n_occ;
-            s.pending = true;
-            return true;
-        }
-        exit_k = 0;
-    } else {
-        s.n_occ_acc += uint32_t(e) + 1u;
-        exit_k = 4 - e;
+    // occupancy_probe counters: e + 1 levels read (5 when level 0 decides).
+    // Written branch-free so every empty point reaches next_step on one path.
+    s.n_occ_acc += uint32_t(e) + 1u;
+    // level-0 bit from the code's child byte (no second dependent load)
+    const uint32_t child = uint32_t(i0[0] & 1) | (uint32_t(i0[1] & 1) << 1) | (uint32_t(i0[2] & 1) << 2);
+    if (e == 4 && ((code >> child) & 1u)) {
+        ++s.n_occ;
+        s.pending = true;
+        return true;
     }
+    const int exit_k = e == 4 ? 0 : 4 - e;
     // next_step (occupancy.hpp:261-276) on the unclamped point ray.at(t). Its
     // voxel_of clamps the index to [0, res-1], so the unclamped point's voxel is
     // the clamped point's: (x+1)*h < 0 <=> x < -1 and (x+1)*h >= res <=> x >= 1.
