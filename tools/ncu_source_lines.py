@@ -1,0 +1,36 @@
+import csv, re, sys, collections, subprocess, os, glob
+lib, rep, fn = sys.argv[1], sys.argv[2], sys.argv[3]
+d = f"/tmp/cmp/{os.path.basename(lib)}"
+os.makedirs(d, exist_ok=True)
+subprocess.run(f"cd {d} && cuobjdump -xelf all {lib} >/dev/null 2>&1", shell=True)
+cub = [c for c in glob.glob(d+"/*.cubin") if "march" in c][0]
+txt = subprocess.run(["nvdisasm","-gi",cub],capture_output=True,text=True).stdout.split("\n")
+start=None
+for i,l in enumerate(txt):
+    if l.startswith("_ZN") and fn in l and l.endswith(":"): start=i;break
+insts=[];cur=None;prev=False
+for l in txt[start+1:]:
+    if l.startswith("\t.section") or l.startswith("//----"): break
+    m=re.match(r'\s*//## File "([^"]+)", line (\d+)(.*)',l)
+    if m and prev: continue
+    prev=bool(m)
+    if m:
+        cur=(m.group(1).split("/")[-1],int(m.group(2))); continue
+    m=re.match(r'\s*/\*([0-9a-f]{4,})\*/\s+(.*)',l)
+    if m: insts.append((m.group(2).strip(),cur))
+csvtxt = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source=sass"],capture_output=True,text=True).stdout
+rows=list(csv.reader(csvtxt.splitlines()))
+hdr=rows[1];data=rows[2:]
+iE=hdr.index("Instructions Executed");iT=hdr.index("Thread Instructions Executed");iS=hdr.index("Warp Stall Sampling (All Samples)")
+print("rows",len(data),"sass",len(insts))
+by=collections.defaultdict(lambda:[0,0,0])
+for k in range(min(len(data),len(insts))):
+    key=insts[k][1] or ("?",0)
+    lab=f"{key[0]}:{key[1]}"
+    by[lab][0]+=int(data[k][iE] or 0);by[lab][1]+=int(data[k][iT] or 0);by[lab][2]+=int(data[k][iS] or 0)
+tot=[sum(v[i] for v in by.values()) for i in range(3)]
+print("warp inst %.3fG thread inst %.3fG"%(tot[0]/1e9,tot[1]/1e9))
+out=sys.argv[4]
+with open(out,"w") as f:
+    for lab,v in sorted(by.items(),key=lambda kv:-kv[1][0]):
+        f.write(f"{lab}\t{v[0]}\t{v[1]}\t{v[2]}\n")
