@@ -78,6 +78,13 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def load_tensor_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text()).get("bf16_tflops", 0.0)) or None
+    return None
+
+
 def algorithmic_bytes(stats, L, b_c=2, b_f=2):
     """sum over rays of occupied*8*((8+2L)*b_c + 8L*b_f)
     + 4*occ_acc + 1*dist_acc + 12 (RGB out)."""
@@ -141,6 +148,11 @@ def cpu_sample(scene_synth, cam, W, H, seconds, kind_pref="reference"):
     kind = "reference" if (kind_pref == "reference" and REF_SO.exists()) else "port"
     cs = CpuScene(scene_synth.desc_ptr, "ref" if kind == "reference" else "oracle")
     threads = os.cpu_count() or 1
+    # one host thread on a small band first (1 thread and nproc)
+    r1 = 4
+    t = time.perf_counter()
+    cs.render(cam, ng.Opts(window=(0, H // 2 - r1 // 2, W, r1)).to_c(), nthreads=1)
+    one_thread_mrays = W * r1 / (time.perf_counter() - t) / 1e6
     rows = 8
     y0 = H // 2 - rows // 2
     t = time.perf_counter()
@@ -153,8 +165,17 @@ def cpu_sample(scene_synth, cam, W, H, seconds, kind_pref="reference"):
     dt = time.perf_counter() - t
     cs.close()
     rays = W * rows
+    model = ""
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                model = l.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     return {"kind": kind, "cores": threads, "rays": rays, "seconds": dt,
             "mrays_per_s": rays / dt / 1e6, "fps": rays / dt / (W * H),
+            "one_thread_mrays_per_s": one_thread_mrays, "cpu_model": model,
             "sample": f"{W}x{rows} band (rows {y0}..{y0 + rows - 1}) of camera 0, {threads} threads"}
 
 
@@ -234,9 +255,11 @@ def run_ours(args):
     for s in range(args.warmup + args.steps):
         c = mg.camera_of(rank, world, s, N_CAMS)
         if c not in alg:
-            _, st = ng.render(scene, [cams[c]], ng.Opts(mlp=args.mlp), stats=True)
+            rgb_c, st = ng.render(scene, [cams[c]], ng.Opts(mlp=args.mlp), stats=True)
             st = st.cpu().numpy()
-            alg[c] = (algorithmic_bytes(st, scene.L, b_store, b_store), st.reshape(-1, 4).mean(0))
+            shaded = int((rgb_c != 0).any(-1).sum().item())  # final_t < 1 rays (the rest are black)
+            alg[c] = (algorithmic_bytes(st, scene.L, b_store, b_store), st.reshape(-1, 4).mean(0),
+                      shaded)
     for s in range(args.warmup):
         step_fn(s)
     torch.cuda.synchronize()
@@ -315,10 +338,26 @@ def run_ours(args):
         peak, peak_src = load_peaks()
         k1_avg = sum(k1_ms) / len(k1_ms)
         achieved = (bytes_k1 / args.steps) / (k1_avg / 1e3) / 1e9
-        traffic = None
+        traffic = l2_traffic = None
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
-            traffic = json.loads(tp.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
+            tj = json.loads(tp.read_text()).get(args.config, {})
+            traffic = tj.get("dram_bytes_per_launch")
+            l2_traffic = tj.get("l2_bytes_per_launch")
+        # also report K1 against the L2 and random-gather ceilings
+        # measured on this B200 (tools/measure_peaks.cu -> profiles/*_peaks.json)
+        ceilings = None
+        pk = sorted((ROOT / "profiles").glob("*_peaks.json"))
+        if pk:
+            pj = json.loads(pk[-1].read_text())
+            ceilings = {k: {"peak_gbs": pj[k], "frac": achieved / pj[k]}
+                        for k in ("l2_read_gbs", "l2_gather32_gbs", "l2_gather16_gbs",
+                                  "hbm_gather32_gbs") if k in pj}
+            ceilings["source"] = f"profiles/{pk[-1].name} ({pj.get('method', '')})"
+        shaded = np.mean([alg[mg.camera_of(rank, world, args.warmup + i, N_CAMS)][2]
+                          for i in range(args.steps)])
+        k2_avg = sum(k2_ms) / len(k2_ms)
+        k2_flop = 11520.0 * shaded  # 11,520 FLOP per shaded ray
         mean_stats = np.mean([alg[mg.camera_of(rank, world, args.warmup + i, N_CAMS)][1]
                               for i in range(args.steps)], axis=0)
         line = {
@@ -343,11 +382,18 @@ def run_ours(args):
                                           "dist_acc": round(float(mean_stats[3]), 2)},
                        "scene_device_bytes": int(info.device_bytes),
                        "parallelism": f"dp{world} (camera sharding, NCCL gather to rank 0)"},
-            "kernel_ms": {"march_K1": k1_avg, "shade_K2": sum(k2_ms) / len(k2_ms)},
+            "kernel_ms": {"march_K1": k1_avg, "shade_K2": k2_avg},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "march_kernel (K1)",
                          "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": bytes_k1 / args.steps},
+                         "algorithmic_bytes_per_launch": bytes_k1 / args.steps,
+                         "l2_traffic": l2_traffic, "other_ceilings": ceilings},
+            "k2_tensor": {"kernel": "shade_tc_kernel (K2)" if args.mlp == "tensor" else "shade_exact_kernel",
+                          "shaded_rays": int(shaded), "flop_per_launch": k2_flop,
+                          "achieved_tflops": k2_flop / (k2_avg * 1e-3) / 1e12,
+                          "peak_tflops": load_tensor_peak(),
+                          "note": "psi FLOP (23-64-64-3); the tensor path issues 3 bf16 products "
+                                  "per FLOP (hi/lo split) and runs layer 3 on CUDA cores"},
             "e2e_sync": {"value": e2e_sync_fps, "unit": UNIT,
                          "api": "ngprt_render_host per frame (pinned host RGB, L2 flushed before each)"},
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 168,
@@ -363,7 +409,9 @@ def run_ours(args):
             cb = cpu_sample(synth, cam_of(0), W, H, args.cpu_seconds)
             line["cpu_baseline"] = {"value": cb["fps"], "unit": UNIT, "cores": cb["cores"],
                                     "kind": cb["kind"], "sample": cb["sample"],
-                                    "mrays_per_s": cb["mrays_per_s"]}
+                                    "mrays_per_s": cb["mrays_per_s"],
+                                    "one_thread_mrays_per_s": cb["one_thread_mrays_per_s"],
+                                    "cpu_model": cb["cpu_model"]}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

@@ -21,6 +21,7 @@ METRICS = [
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("lts__t_bytes.sum", "L2 bytes"),
+    ("lts__t_sectors.sum", "L2 sectors (32 B)"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
@@ -90,7 +91,7 @@ def main():
     lines = [f"# ncu summary `{tag}`", "",
              f"Source: `{rep.name}` (`ncu --set full --clock-control none`, cold L2 per replay) and "
              f"`{launches.name}` (`--metrics gpu__time_duration.sum`, every launch).", ""]
-    traffic = None
+    traffic = l2 = None
     for row in data:
         name = row[h.index("Kernel Name")]
         short = name.split("(")[0].replace("void ", "").replace("ngprt_dev::<unnamed>::", "").replace("unnamed>::", "")
@@ -106,6 +107,12 @@ def main():
             i, j = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
             traffic = (float(row[i]) * UNIT_SCALE.get(units[i], 1) +
                        float(row[j]) * UNIT_SCALE.get(units[j], 1))
+            l2 = None
+            if "lts__t_bytes.sum" in h:
+                k = h.index("lts__t_bytes.sum")
+                l2 = float(row[k]) * UNIT_SCALE.get(units[k], 1)
+            elif "lts__t_sectors.sum" in h:  # 32 B sectors
+                l2 = float(row[h.index("lts__t_sectors.sum")]) * 32.0
         st = stalls(rep, short.split("<")[0].split("::")[-1])
         if st:
             lines.append("")
@@ -122,8 +129,8 @@ def main():
     if traffic is not None:
         tp = HERE / "ncu_traffic.json"
         d = json.loads(tp.read_text()) if tp.exists() else {}
-        d[config] = {"dram_bytes_per_launch": traffic, "source": f"{rep.name} ({tag})",
-                     "kernel": "march_kernel (K1)"}
+        d[config] = {"dram_bytes_per_launch": traffic, "l2_bytes_per_launch": l2,
+                     "source": f"{rep.name} ({tag})", "kernel": "march_kernel (K1)"}
         tp.write_text(json.dumps(d, indent=1) + "\n")
     print((HERE / f"{tag}_kernels.md").read_text())
 
