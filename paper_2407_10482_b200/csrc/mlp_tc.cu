@@ -16,6 +16,8 @@
 //   4. layer 3 (64 -> 3) runs on CUDA cores from TMEM, then
 //      rgb = sigmoid(C_d + out) with the glibc-expf sigmoid; rays with
 //      final_t == 1 stay black.
+#include <cuda_bf16.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -40,6 +42,7 @@ constexpr int kOffW1h = 0, kOffW1l = kOffW1h + kW1Bytes, kOffW2h = kOffW1l + kW1
 // f32 tail: b0[64], b1[64], W2[3][64], b2[3] (+1 pad)
 constexpr int kF32Count = 64 + 64 + 192 + 4;
 constexpr int kImageBytes = kOffF32 + kF32Count * 4;
+static_assert(sizeof(ShadeConsts) == kF32Count * 4, "ShadeConsts mirrors the image's f32 tail");
 // activations: hi/lo planes of a 128 x 64 tile (layer 1 uses the first K = 32 part)
 constexpr int kActBytes = kM * kH * 2;                 // 16384 per plane
 constexpr int kSmemBytes = kImageBytes + 2 * kActBytes + 64;
@@ -122,7 +125,8 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
     for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Store one row of K values as bf16 hi/lo into the two canonical planes.
+// Store one row of K values as bf16 hi/lo into the two canonical planes
+// (hardware round-to-nearest-even pair conversions, F2FP.BF16.F32.PACK_AB).
 template <int K>
 __device__ __forceinline__ void store_row_split(uint8_t* hi, uint8_t* lo, int row, const float* x) {
 #pragma unroll
@@ -131,10 +135,11 @@ __device__ __forceinline__ void store_row_split(uint8_t* hi, uint8_t* lo, int ro
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const float a = x[8 * c + 2 * j], b = x[8 * c + 2 * j + 1];
-            const uint16_t ah = f2bf(a), bh = f2bf(b);
-            const uint16_t al = f2bf(a - bf2f(ah)), bl = f2bf(b - bf2f(bh));
-            h[j] = uint32_t(ah) | (uint32_t(bh) << 16);
-            l[j] = uint32_t(al) | (uint32_t(bl) << 16);
+            const __nv_bfloat162 hb = __floats2bfloat162_rn(a, b);
+            const float2 hf = __bfloat1622float2(hb);
+            const __nv_bfloat162 lb = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+            h[j] = *reinterpret_cast<const uint32_t*>(&hb);
+            l[j] = *reinterpret_cast<const uint32_t*>(&lb);
         }
         const uint32_t off = canon_off(row, 8 * c, K);
         *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
@@ -159,8 +164,8 @@ __device__ __forceinline__ void issue_layer(uint32_t d_tmem, uint32_t a_hi, uint
 }
 
 __global__ void __launch_bounds__(kThreads, 3)
-    shade_tc_kernel(const uint8_t* __restrict__ image, const RayAcc* __restrict__ acc,
-                    float* __restrict__ rgb, size_t n_rays) {
+    shade_tc_kernel(const uint8_t* __restrict__ image, const __grid_constant__ ShadeConsts C,
+                    const RayAcc* __restrict__ acc, float* __restrict__ rgb, size_t n_rays) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w_img = smem;
     uint8_t* act_hi = smem + kImageBytes;
@@ -190,11 +195,12 @@ __global__ void __launch_bounds__(kThreads, 3)
     const uint32_t tmem = *tmem_slot;
     const uint32_t d1 = tmem, d2 = tmem + kH;                 // column offsets
     const uint32_t lane_base = uint32_t(warp * 32) << 16;     // this warp's TMEM lanes
-    const float* f32 = reinterpret_cast<const float*>(w_img + kOffF32);
-    const float* b0 = f32;
-    const float* b1 = f32 + 64;
-    const float* w2 = f32 + 128;
-    const float* b2 = f32 + 320;
+    // biases and the 64 -> 3 layer come from the kernel parameter (constant bank):
+    // with the loops unrolled each is an FFMA/FADD operand, no shared-memory load
+    const float* b0 = C.b0;
+    const float* b1 = C.b1;
+    const float* w2 = C.w2;
+    const float* b2 = C.b2;
     const uint32_t s_w = uint32_t(__cvta_generic_to_shared(w_img));
     const uint32_t s_ahi = uint32_t(__cvta_generic_to_shared(act_hi));
     const uint32_t s_alo = uint32_t(__cvta_generic_to_shared(act_lo));
@@ -322,8 +328,16 @@ void pack_psi_tc(const float* psi, void* out_v) {
     std::memcpy(f + 320, psi + kPsiB2, 3 * 4);
 }
 
-void launch_shade_tensor(const DevScene&, const void* psi_tc, const RayAcc* acc, float* rgb,
-                         size_t n_rays, cudaStream_t st) {
+void shade_consts_from_psi(const float* psi, ShadeConsts* c) {
+    std::memcpy(c->b0, psi + kPsiB0, 64 * 4);
+    std::memcpy(c->b1, psi + kPsiB1, 64 * 4);
+    std::memcpy(c->w2, psi + kPsiW2, 192 * 4);
+    std::memcpy(c->b2, psi + kPsiB2, 3 * 4);
+    c->b2[3] = 0.f;
+}
+
+void launch_shade_tensor(const DevScene&, const void* psi_tc, const ShadeConsts& consts,
+                         const RayAcc* acc, float* rgb, size_t n_rays, cudaStream_t st) {
     if (!n_rays) return;
     static int grid = 0;
     if (!grid) {
@@ -356,7 +370,7 @@ void launch_shade_tensor(const DevScene&, const void* psi_tc, const RayAcc* acc,
     const size_t tiles = (n_rays + kM - 1) / kM;
     const int blocks = int(tiles < size_t(grid) ? tiles : size_t(grid));
     shade_tc_kernel<<<blocks, kThreads, kSmemBytes, st>>>(
-        static_cast<const uint8_t*>(psi_tc), acc, rgb, n_rays);
+        static_cast<const uint8_t*>(psi_tc), consts, acc, rgb, n_rays);
 }
 
 }  // namespace ngprt_dev

@@ -54,6 +54,7 @@ struct ngprt_scene {
     DevScene ds{};
     std::vector<void*> allocs;
     void* psi_tc = nullptr;
+    ShadeConsts shade_consts{};
     ngprt_scene_info info{};
     void* fine_block = nullptr;
     size_t fine_block_bytes = 0;
@@ -401,6 +402,7 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         ds.psi = g;
         std::vector<unsigned char> tc(psi_tc_bytes());
         pack_psi_tc(packed.data(), tc.data());
+        shade_consts_from_psi(packed.data(), &s->shade_consts);
         NG_TRY(s->alloc(&s->psi_tc, tc.size()));
         NG_TRY(cudaMemcpyAsync(s->psi_tc, tc.data(), tc.size(), cudaMemcpyHostToDevice, st));
         NG_TRY(cudaStreamSynchronize(st));
@@ -562,7 +564,7 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         if (o->mlp_mode == NGPRT_MLP_EXACT)
             launch_shade_exact(s->ds, acc, out, per_cam * nc, st);
         else
-            launch_shade_tensor(s->ds, s->psi_tc, acc, out, per_cam * nc, st);
+            launch_shade_tensor(s->ds, s->psi_tc, s->shade_consts, acc, out, per_cam * nc, st);
         if (o->profile) {
             cudaEventRecord(s->prof_event(3 * li + 2), st);
             s->prof_launches = li + 1;

@@ -38,8 +38,14 @@ void launch_probe_codes(const DevScene& sc, uint16_t* out, cudaStream_t st);
 // K2 (exact): f32 CUDA-core deferred MLP in the reference's operation order.
 void launch_shade_exact(const DevScene& sc, const RayAcc* acc, float* rgb, size_t n_rays,
                         cudaStream_t st);
+// psi's biases and 64 -> 3 layer, passed to K2 as a kernel parameter.
+struct ShadeConsts {
+    float b0[64], b1[64], w2[192], b2[4];
+};
+void shade_consts_from_psi(const float* psi_host_packed, ShadeConsts* out);
 // K2 (tensor): tcgen05 deferred MLP, 128 rays per CTA tile.
-void launch_shade_tensor(const DevScene& sc, const void* psi_tc, const RayAcc* acc, float* rgb,
+void launch_shade_tensor(const DevScene& sc, const void* psi_tc, const ShadeConsts& consts,
+                         const RayAcc* acc, float* rgb,
                          size_t n_rays, cudaStream_t st);
 // Packs psi into the tcgen05 operand layout (done once per scene).
 size_t psi_tc_bytes();
