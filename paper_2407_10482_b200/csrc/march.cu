@@ -502,7 +502,13 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
             const int j2 = j + jstep;
             const bool two = j2 < 2 * L;
             const float y0 = activate_sigmoid(scr[j * kBlock], tab);
-            const float y1 = activate_sigmoid(two ? scr[j2 * kBlock] : 0.0f, tab);
+            float y1;
+            if (FC && jstep == 1) {  // a beta logit: colour only, tensor mode -> fast sigmoid
+                const float v = two ? scr[j2 * kBlock] : 0.0f;
+                y1 = __fdividef(1.0f, 1.0f + __expf(-v));
+            } else {
+                y1 = activate_sigmoid(two ? scr[j2 * kBlock] : 0.0f, tab);
+            }
             scr[j * kBlock] = y0;
             if (two) scr[j2 * kBlock] = y1;
         }
