@@ -85,21 +85,8 @@ public:
     Image render(const PosedDataset& ds, size_t frame, const RenderOptions& o = {},
                  std::vector<MarchCounters>* counters = nullptr) const {
         if (frame >= ds.frames.size()) throw std::out_of_range("render: bad frame index");
-        ngprt_camera cam{};
-        for (int i = 0; i < 16; ++i) cam.c2w[i] = ds.frames[frame].c2w[i];
-        cam.fx = ds.fx;
-        cam.fy = ds.fy;
-        cam.cx = ds.cx;
-        cam.cy = ds.cy;
-        cam.width = uint32_t(ds.width);
-        cam.height = uint32_t(ds.height);
-        ngprt_render_opts ro{};
-        ro.step = o.step;
-        ro.use_dist_grid = o.use_dist_grid;
-        ro.max_step_rule = o.max_step_rule;
-        ro.early_stop = o.early_stop;
-        ro.keep_level = int8_t(o.keep_level);
-        ro.mlp_mode = o.exact_mlp ? NGPRT_MLP_EXACT : NGPRT_MLP_TENSOR;
+        const ngprt_camera cam = camera_of(ds, frame);
+        const ngprt_render_opts ro = opts_of(o);
         Image img(ds.width, ds.height);
         std::vector<ngprt_ray_stats> st(counters ? size_t(ds.width) * ds.height : 0);
         check(ngprt_render_host(h_, &cam, 1, &ro, img.rgb.data(), counters ? st.data() : nullptr),
@@ -116,9 +103,45 @@ public:
         return img;
     }
 
+    // Serving: enqueue frame `frame` into `img` (sized ds.width x ds.height) and
+    // return; the device->host copy overlaps the next enqueued frame's march
+    // (ngprt_render_host_async). `img` must stay alive until wait().
+    void render_async(const PosedDataset& ds, size_t frame, Image& img,
+                      const RenderOptions& o = {}) const {
+        if (frame >= ds.frames.size()) throw std::out_of_range("render: bad frame index");
+        if (img.width != ds.width || img.height != ds.height) img = Image(ds.width, ds.height);
+        const ngprt_camera cam = camera_of(ds, frame);
+        const ngprt_render_opts ro = opts_of(o);
+        check(ngprt_render_host_async(h_, &cam, 1, &ro, img.rgb.data(), nullptr),
+              "ngprt_render_host_async");
+    }
+    void wait() const { check(ngprt_render_host_wait(h_), "ngprt_render_host_wait"); }
+
     ngprt_scene* handle() const { return h_; }
 
 private:
+    static ngprt_camera camera_of(const PosedDataset& ds, size_t frame) {
+        ngprt_camera cam{};
+        for (int i = 0; i < 16; ++i) cam.c2w[i] = ds.frames[frame].c2w[i];
+        cam.fx = ds.fx;
+        cam.fy = ds.fy;
+        cam.cx = ds.cx;
+        cam.cy = ds.cy;
+        cam.width = uint32_t(ds.width);
+        cam.height = uint32_t(ds.height);
+        return cam;
+    }
+    static ngprt_render_opts opts_of(const RenderOptions& o) {
+        ngprt_render_opts ro{};
+        ro.step = o.step;
+        ro.use_dist_grid = o.use_dist_grid;
+        ro.max_step_rule = o.max_step_rule;
+        ro.early_stop = o.early_stop;
+        ro.keep_level = int8_t(o.keep_level);
+        ro.mlp_mode = o.exact_mlp ? NGPRT_MLP_EXACT : NGPRT_MLP_TENSOR;
+        return ro;
+    }
+
     ngprt_scene* h_ = nullptr;
 };
 

@@ -149,14 +149,25 @@ int main() {
                                 ref_mc[i].occ_grid_accesses != gpu_mc[i].occ_grid_accesses ||
                                 ref_mc[i].dist_grid_accesses != gpu_mc[i].dist_grid_accesses;
     }
+    // serving path: every frame enqueued, one wait; equals the synchronous render
+    long async_mismatch = 0;
+    {
+        std::vector<Image> imgs(ds.frames.size());
+        for (size_t f = 0; f < ds.frames.size(); ++f) gs.render_async(ds, f, imgs[f]);
+        gs.wait();
+        for (size_t f = 0; f < ds.frames.size(); ++f) {
+            const Image sync = gs.render(ds, f);
+            async_mismatch += max_abs_diff(sync, imgs[f]) != 0.0;
+        }
+    }
     ngprt_scene_info info{};
     ngprt_scene_info_get(gs.handle(), &info);
     size_t bake_corners = 0;
     const bool bake_same = bake_identical(&bake_corners);
     std::printf("{\"frames\": %zu, \"max_abs_exact\": %.9g, \"max_abs_tensor\": %.9g, "
                 "\"psnr_tensor\": %.3f, \"counter_mismatch\": %ld, \"storage\": %d, "
-                "\"bake_identical\": %s, \"bake_corners\": %zu}\n",
+                "\"bake_identical\": %s, \"bake_corners\": %zu, \"async_mismatch\": %ld}\n",
                 ds.frames.size(), worst_exact, worst_tc, min_psnr_tc, counter_mismatch,
-                int(info.storage), bake_same ? "true" : "false", bake_corners);
+                int(info.storage), bake_same ? "true" : "false", bake_corners, async_mismatch);
     return 0;
 }

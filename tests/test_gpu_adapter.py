@@ -31,3 +31,5 @@ def test_adapter_renders_reference_baked_scene():
     # ngprt::gpu::bake over a reference NgpRtModel == the reference's bake(), file for file
     assert r["bake_identical"] is True
     assert r["bake_corners"] > 0
+    # ngprt::gpu::Scene::render_async + wait (ngprt_render_host_async) == render
+    assert r["async_mismatch"] == 0
