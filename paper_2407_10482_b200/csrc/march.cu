@@ -700,39 +700,48 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
         // (MUFU.RCP, a few ulp) picks it and one exact division evaluates it. Axes
         // within 2^-16 relative of the approximate minimum (near-ties, or anything
         // non-finite) are all evaluated exactly; the result is the reference's.
+        constexpr float kBig = 3.402823466e38f;
         float num[3], q[3];
-        float qmin = 3.402823466e38f;
-        int amin = -1;
+        bool finite = true;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const float d = s.ray.d[a];
-            const float v2 = 2.0f * float(iu[a] >> exit_k);
-            // T(extent)*T(v)/T(res): a power-of-two divisor is an exact reciprocal multiply
-            const float lo = -1.0f + (sc.occ_pow2 ? v2 * sc.lvl_inv_res[exit_k] : v2 / float(res));
-            const float hi = lo + sc.lvl_two_over_res[exit_k];
-            num[a] = (d > 0.0f ? hi : lo) - s.ray.o[a];
+            const int v = iu[a] >> exit_k;
+            float bound;
+            if (sc.occ_pow2) {
+                // lo = -1 + 2v/res and hi = lo + 2/res are exact for a power-of-two res
+                // (multiples of 2/res in [-1, 1]), so bound = -1 + (v + [d > 0]) * (2/res)
+                // is one exactly-rounded FMA with the same value
+                bound = __fmaf_rn(float(v + (d > 0.0f ? 1 : 0)), sc.lvl_two_over_res[exit_k], -1.0f);
+            } else {
+                const float lo = -1.0f + (2.0f * float(v)) / float(res);
+                bound = d > 0.0f ? lo + sc.lvl_two_over_res[exit_k] : lo;
+            }
+            num[a] = bound - s.ray.o[a];
             float rd;
             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d));
-            q[a] = (d == 0.0f) ? 3.402823466e38f : num[a] * rd;
-            if (d != 0.0f && !(q[a] >= qmin)) {  // NaN-safe argmin
-                qmin = q[a];
-                amin = a;
-            }
+            q[a] = (d == 0.0f) ? kBig : num[a] * rd;
+            finite = finite && (d == 0.0f || fabsf(q[a]) < 3.0e38f);
         }
-        float t_exit = 3.402823466e38f;
-        if (amin >= 0) {
-            const float dsel = amin == 0 ? s.ray.d[0] : (amin == 1 ? s.ray.d[1] : s.ray.d[2]);
-            const float nsel = amin == 0 ? num[0] : (amin == 1 ? num[1] : num[2]);
-            const float tc = nsel / dsel;
-            t_exit = (tc < t_exit) ? tc : t_exit;
-            const float margin = fabsf(qmin) * 1.52587890625e-5f + 1e-30f;  // 2^-16
+        // smallest approximate ratio, its axis, and the second smallest
+        const float m01 = fminf(q[0], q[1]), x01 = fmaxf(q[0], q[1]);
+        const float qmin = fminf(m01, q[2]), q2nd = fminf(x01, fmaxf(m01, q[2]));
+        const int amin = (q[0] <= q[1] && q[0] <= q[2]) ? 0 : (q[1] <= q[2] ? 1 : 2);
+        float t_exit = kBig;
+        const bool tie = !finite || !(q2nd > qmin + (fabsf(qmin) * 1.52587890625e-5f + 1e-30f));
+        if (!tie) {
+            if (qmin < kBig) {  // else every d == 0: t_exit stays max (the reference's start)
+                const float dsel = amin == 0 ? s.ray.d[0] : (amin == 1 ? s.ray.d[1] : s.ray.d[2]);
+                const float nsel = amin == 0 ? num[0] : (amin == 1 ? num[1] : num[2]);
+                t_exit = nsel / dsel;
+            }
+        } else {  // near-tie or non-finite: every axis exactly, as the reference
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                if (a == amin || s.ray.d[a] == 0.0f) continue;
-                if (!(q[a] > qmin + margin) || !(fabsf(q[a]) < 3.0e38f)) {  // near-tie: exact too
-                    const float tc2 = num[a] / s.ray.d[a];
-                    t_exit = (tc2 < t_exit) ? tc2 : t_exit;
-                }
+                const float d = s.ray.d[a];
+                if (d == 0.0f) continue;
+                const float tc = num[a] / d;
+                t_exit = (tc < t_exit) ? tc : t_exit;
             }
         }
         float sz = t_exit - s.t;
