@@ -101,6 +101,12 @@ __device__ __forceinline__ int voxel_1d(float x, float h, int res) {
     const int i = __float2int_rd((x - (-1.0f)) * h);  // == int(floor(u)) for finite u
     return i < 0 ? 0 : (i > res - 1 ? res - 1 : i);
 }
+// Same for a point already clamped to [-1, 1]: u = (x + 1) * h >= +0, so only
+// the upper clamp (x == 1 -> u == res) can apply.
+__device__ __forceinline__ int voxel_1d_clamped(float x, float h, int res) {
+    const int i = __float2int_rd((x - (-1.0f)) * h);
+    return i > res - 1 ? res - 1 : i;
+}
 
 // Stencil along one axis: base index and fractional offset (hash_grid.hpp:38-46).
 __device__ __forceinline__ void stencil_axis(float x, float h, int res, int& base, float& frac) {
@@ -623,12 +629,11 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
     s.has_ray = true;
 }
 
-// Probe-code layout: 4x4x4 bricks of level-1 voxels (128 B = one L1 line,
-// 4x4x1 per 32 B sector), bricks x-fastest. Lanes of a warp sit at different
-// depths of neighbouring rays and a lane's successive points move in any
-// direction, so a brick keeps more of them in one line than x-major rows do.
+// Probe-code layout: x-major (default) or 4x4x4 bricks of level-1 voxels
+// (128 B = one L1 line). Bricks measured neutral on B200, and x-major costs
+// fewer index instructions per marching point.
 #ifndef NGPRT_PROBE_BRICK
-#define NGPRT_PROBE_BRICK 1
+#define NGPRT_PROBE_BRICK 0
 #endif
 __device__ __forceinline__ uint32_t probe_index(uint32_t x, uint32_t y, uint32_t z, uint32_t r1) {
 #if NGPRT_PROBE_BRICK
@@ -654,7 +659,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     const int r0 = sc.occ_res[0], r1 = sc.occ_res[1];
     int i0[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) i0[a] = voxel_1d(s.xc[a], sc.occ_h0, r0);
+    for (int a = 0; a < 3; ++a) i0[a] = voxel_1d_clamped(s.xc[a], sc.occ_h0, r0);
     // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
     const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
     const uint32_t code = __ldg(sc.probe + pidx);
@@ -683,8 +688,9 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
             g = code & 0xffu;  // the probe code's own level-1 voxel (iu >> 1 == pidx's voxel)
         } else {
             const int gr = sc.dist_res;
-            const int vx = voxel_1d(s.xc[0], sc.dist_h, gr), vy = voxel_1d(s.xc[1], sc.dist_h, gr),
-                      vz = voxel_1d(s.xc[2], sc.dist_h, gr);
+            const int vx = voxel_1d_clamped(s.xc[0], sc.dist_h, gr),
+                      vy = voxel_1d_clamped(s.xc[1], sc.dist_h, gr),
+                      vz = voxel_1d_clamped(s.xc[2], sc.dist_h, gr);
             g = __ldg(sc.dist + (size_t(vx) + size_t(gr) * (size_t(vy) + size_t(gr) * vz)));
         }
     }
