@@ -610,7 +610,8 @@ __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s
 __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, uint32_t slot,
                                           Lane& s) {
     const uint32_t cam = tile / p.tiles_per_cam, tt = tile % p.tiles_per_cam;
-    const uint32_t px = (tt % p.tiles_x) * 8 + (slot & 7), py = (tt / p.tiles_x) * 4 + (slot >> 3);
+    const uint32_t px = (tt % p.tiles_x) * kRayTileW + (slot % kRayTileW),
+                   py = (tt / p.tiles_x) * kRayTileH + (slot / kRayTileW);
     s.has_ray = false;
     if (px >= p.w || py >= p.h) return;
     s.out_idx = (cam * p.h + py) * p.w + px;

@@ -533,8 +533,8 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         }();
         p.fast_color = (o->mlp_mode == NGPRT_MLP_TENSOR) && fast_color;
     }
-    p.tiles_x = (W + 7) / 8;
-    p.tiles_per_cam = p.tiles_x * ((H + 3) / 4);
+    p.tiles_x = (W + kRayTileW - 1) / kRayTileW;
+    p.tiles_per_cam = p.tiles_x * ((H + kRayTileH - 1) / kRayTileH);
     std::unique_lock<std::mutex> prof_lock(s->prof_mu, std::defer_lock);
     if (o->profile) {
         prof_lock.lock();

@@ -14,6 +14,11 @@ struct CamParams {
 
 constexpr int kMaxCamsPerLaunch = 64;  // 64 x 136 B of kernel parameters (CUDA >= 12.1)
 constexpr int kTileW = 16, kTileH = 8, kBlock = kTileW * kTileH;
+// K1 ray tile: the 32 rays a warp takes at a time (kRayTileW x kRayTileH pixels)
+#ifndef NGPRT_RAY_TILE_W
+#define NGPRT_RAY_TILE_W 4
+#endif
+constexpr int kRayTileW = NGPRT_RAY_TILE_W, kRayTileH = 32 / NGPRT_RAY_TILE_W;
 
 struct MarchParams {
     CamParams cams[kMaxCamsPerLaunch];
