@@ -1,3 +1,9 @@
+"""Join an ncu source-page capture (SASS, per-instruction metrics) with nvdisasm
+line info, aggregating warp instructions / thread instructions / stall samples
+per source line of one kernel.
+
+  python tools/ncu_source_lines.py <lib.so> <report.ncu-rep> <mangled-name-fragment> <out.tsv>
+"""
 import csv, re, sys, collections, subprocess, os, glob
 lib, rep, fn = sys.argv[1], sys.argv[2], sys.argv[3]
 d = f"/tmp/cmp/{os.path.basename(lib)}"
@@ -20,7 +26,19 @@ for l in txt[start+1:]:
     if m: insts.append((m.group(2).strip(),cur))
 csvtxt = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source=sass"],capture_output=True,text=True).stdout
 rows=list(csv.reader(csvtxt.splitlines()))
-hdr=rows[1];data=rows[2:]
+# the source page lists one block per profiled kernel: '"Kernel Name",<name>' then a header row
+blocks=[]
+for i,r in enumerate(rows):
+    if r and r[0]=="Kernel Name": blocks.append(i)
+blocks.append(len(rows))
+sel=None
+for bi in range(len(blocks)-1):
+    name=rows[blocks[bi]][1] if len(rows[blocks[bi]])>1 else ""
+    plain=fn.split("ILi")[0]
+    if plain in name.replace(" ","") or plain in name:
+        sel=(blocks[bi],blocks[bi+1]); break
+if sel is None: sel=(blocks[0],blocks[1])
+hdr=rows[sel[0]+1];data=rows[sel[0]+2:sel[1]]
 iE=hdr.index("Instructions Executed");iT=hdr.index("Thread Instructions Executed");iS=hdr.index("Warp Stall Sampling (All Samples)")
 print("rows",len(data),"sass",len(insts))
 by=collections.defaultdict(lambda:[0,0,0])
