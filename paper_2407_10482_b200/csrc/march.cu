@@ -429,12 +429,18 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
 #ifndef NGPRT_FINE_PREFETCH
 #define NGPRT_FINE_PREFETCH 1
 #endif
+#ifndef NGPRT_FINE1_ASYNC
+#define NGPRT_FINE1_ASYNC 1
+#endif
 template <int L, bool FC>
 __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const float x[3],
                                                   int keep_level, const unsigned long long* tab,
-                                                  float* scr, float out[8]) {
+                                                  float* scr, uint4* stage, float out[8]) {
     constexpr int W = 8 + 2 * L;
     constexpr int P = NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L;
+    // fine level P's rows go to shared memory with cp.async (no registers held
+    // while in flight), issued together with the coarse and level-0 rows
+    constexpr bool kAsync = NGPRT_FINE1_ASYNC && P < L;
 #ifndef NGPRT_COARSE_FULL_ROW
 #define NGPRT_COARSE_FULL_ROW 0
 #endif
@@ -463,6 +469,25 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
             craw[k][0] = a.x; craw[k][1] = a.y; craw[k][2] = a.z; craw[k][3] = a.w;
             craw[k][4] = b.x; craw[k][5] = b.y;
         }
+    }
+    // ---- issue: fine level P -> shared memory (cp.async), weights kept ----
+    float fa[3];
+    if constexpr (kAsync) {
+        int b[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[P], sc.fine_res[P], b[a], fa[a]);
+        const uint32_t mask = sc.fine_mask[P];
+        const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
+        const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
+        const uint4* table = reinterpret_cast<const uint4*>(sc.fine[P]);
+        const uint32_t s0 = uint32_t(__cvta_generic_to_shared(stage));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint4* src = table + ((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;"
+                         :: "r"(s0 + uint32_t(k * kBlock * 16)), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     // ---- issue: fine levels 0..P-1 ----
     uint4 fraw[P][8];
@@ -560,9 +585,38 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
         for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
     }
+    // ---- level P from shared memory ----
+    if constexpr (kAsync) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        float w[8];
+        corner_weights(fa, w);
+        float fine[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) fine[c] = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint4 r = stage[k * kBlock];
+            const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 v = __half22float2(h[i]);
+                fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
+                fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
+            }
+        }
+        if (keep_level > 0 && P + 1 != keep_level) {
+#pragma unroll
+            for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
+        }
+        float wo, wb;
+        weights(P, wo, wb);
+        out[0] += wo * fine[0];
+#pragma unroll
+        for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
+    }
     // ---- remaining levels one round trip each ----
 #pragma unroll 1
-    for (int l = P; l < L; ++l) {
+    for (int l = kAsync ? P + 1 : P; l < L; ++l) {
         float fine[8];
         fine_level<true, FC>(sc, l, x, fine);
         if (keep_level > 0 && l + 1 != keep_level) {
@@ -769,9 +823,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
     __shared__ float scratch[kBlock * (MLPF ? 8 * L : 8)];
+    __shared__ uint4 fstage[(F16 && !MLPF && L >= 2) ? 8 * kBlock : 1];  // cp.async fine rows
     load_exp_table(tab);
     __syncthreads();
     float* scr = scratch + threadIdx.x;  // element j at scr[j * kBlock]: conflict-free banks
+    uint4* stage = fstage + ((F16 && !MLPF && L >= 2) ? threadIdx.x : 0);
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned lt_mask = (1u << lane) - 1u;
     const uint32_t total_tiles = p.tiles_per_cam * uint32_t(p.n_cams);
@@ -818,7 +874,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
                 float f[8];
                 if constexpr (F16 && !MLPF) {
                     if (sc.fast_decode)
-                        decode_point_fast<L, FC>(sc, s.xc, p.keep_level, tab, scr, f);
+                        decode_point_fast<L, FC>(sc, s.xc, p.keep_level, tab, scr, stage, f);
                     else
                         decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
                 } else {
