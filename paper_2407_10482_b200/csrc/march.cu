@@ -429,8 +429,8 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
 #ifndef NGPRT_FINE_PREFETCH
 #define NGPRT_FINE_PREFETCH 1
 #endif
-#ifndef NGPRT_FINE1_ASYNC
-#define NGPRT_FINE1_ASYNC 1
+#ifndef NGPRT_FINE_ASYNC_LEVELS
+#define NGPRT_FINE_ASYNC_LEVELS 1
 #endif
 template <int L, bool FC>
 __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const float x[3],
@@ -438,9 +438,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
                                                   float* scr, uint4* stage, float out[8]) {
     constexpr int W = 8 + 2 * L;
     constexpr int P = NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L;
-    // fine level P's rows go to shared memory with cp.async (no registers held
-    // while in flight), issued together with the coarse and level-0 rows
-    constexpr bool kAsync = NGPRT_FINE1_ASYNC && P < L;
+    // fine levels P .. P+A-1 go to shared memory with cp.async (no registers held
+    // while in flight), issued together with the coarse and register-held rows
+    constexpr int A = (L - P) < NGPRT_FINE_ASYNC_LEVELS ? (L - P) : NGPRT_FINE_ASYNC_LEVELS;
 #ifndef NGPRT_COARSE_FULL_ROW
 #define NGPRT_COARSE_FULL_ROW 0
 #endif
@@ -470,28 +470,30 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
             craw[k][4] = b.x; craw[k][5] = b.y;
         }
     }
-    // ---- issue: fine level P -> shared memory (cp.async), weights kept ----
-    float fa[3];
-    if constexpr (kAsync) {
+    // ---- issue: fine levels P..P+A-1 -> shared memory (cp.async), weights kept ----
+    float fa[A > 0 ? A : 1][3];
+#pragma unroll
+    for (int j = 0; j < A; ++j) {
+        const int l = P + j;
         int b[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[P], sc.fine_res[P], b[a], fa[a]);
-        const uint32_t mask = sc.fine_mask[P];
+        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[l], sc.fine_res[l], b[a], fa[j][a]);
+        const uint32_t mask = sc.fine_mask[l];
         const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
         const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
-        const uint4* table = reinterpret_cast<const uint4*>(sc.fine[P]);
-        const uint32_t s0 = uint32_t(__cvta_generic_to_shared(stage));
+        const uint4* table = reinterpret_cast<const uint4*>(sc.fine[l]);
+        const uint32_t s0 = uint32_t(__cvta_generic_to_shared(stage + j * 8 * kBlock));
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const uint4* src = table + ((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;"
                          :: "r"(s0 + uint32_t(k * kBlock * 16)), "l"(src) : "memory");
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    if constexpr (A > 0) asm volatile("cp.async.commit_group;" ::: "memory");
     // ---- issue: fine levels 0..P-1 ----
-    uint4 fraw[P][8];
-    float ff[P][3];
+    uint4 fraw[P > 0 ? P : 1][8];
+    float ff[P > 0 ? P : 1][3];
 #pragma unroll
     for (int l = 0; l < P; ++l) {
         int b[3];
@@ -585,17 +587,19 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
         for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
     }
-    // ---- level P from shared memory ----
-    if constexpr (kAsync) {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // ---- levels P..P+A-1 from shared memory ----
+    if constexpr (A > 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < A; ++j) {
+        const int l = P + j;
         float w[8];
-        corner_weights(fa, w);
+        corner_weights(fa[j], w);
         float fine[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) fine[c] = 0.0f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const uint4 r = stage[k * kBlock];
+            const uint4 r = stage[(j * 8 + k) * kBlock];
             const __half2* h = reinterpret_cast<const __half2*>(&r);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -604,19 +608,19 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
                 fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
             }
         }
-        if (keep_level > 0 && P + 1 != keep_level) {
+        if (keep_level > 0 && l + 1 != keep_level) {
 #pragma unroll
             for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
         }
         float wo, wb;
-        weights(P, wo, wb);
+        weights(l, wo, wb);
         out[0] += wo * fine[0];
 #pragma unroll
         for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
     }
     // ---- remaining levels one round trip each ----
 #pragma unroll 1
-    for (int l = kAsync ? P + 1 : P; l < L; ++l) {
+    for (int l = P + A; l < L; ++l) {
         float fine[8];
         fine_level<true, FC>(sc, l, x, fine);
         if (keep_level > 0 && l + 1 != keep_level) {
@@ -823,11 +827,15 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
     __shared__ float scratch[kBlock * (MLPF ? 8 * L : 8)];
-    __shared__ uint4 fstage[(F16 && !MLPF && L >= 2) ? 8 * kBlock : 1];  // cp.async fine rows
+    constexpr int kStageLv = (F16 && !MLPF)
+        ? ((L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) < NGPRT_FINE_ASYNC_LEVELS
+               ? (L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) : NGPRT_FINE_ASYNC_LEVELS)
+        : 0;
+    __shared__ uint4 fstage[kStageLv > 0 ? kStageLv * 8 * kBlock : 1];  // cp.async fine rows
     load_exp_table(tab);
     __syncthreads();
     float* scr = scratch + threadIdx.x;  // element j at scr[j * kBlock]: conflict-free banks
-    uint4* stage = fstage + ((F16 && !MLPF && L >= 2) ? threadIdx.x : 0);
+    uint4* stage = fstage + (kStageLv > 0 ? threadIdx.x : 0);
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned lt_mask = (1u << lane) - 1u;
     const uint32_t total_tiles = p.tiles_per_cam * uint32_t(p.n_cams);
