@@ -785,8 +785,10 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
             num[a] = bound - s.ray.o[a];
             float rd;
             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d));
-            q[a] = (d == 0.0f) ? kBig : num[a] * rd;
-            finite = finite && (d == 0.0f || fabsf(q[a]) < 3.0e38f);
+            // d == 0: rcp.approx gives inf, so q is inf or NaN and the axis goes to the
+            // exact path below, which skips it as the reference does
+            q[a] = num[a] * rd;
+            finite = finite && fabsf(q[a]) < 3.0e38f;
         }
         // smallest approximate ratio, its axis, and the second smallest
         const float m01 = fminf(q[0], q[1]), x01 = fmaxf(q[0], q[1]);
