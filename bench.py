@@ -392,6 +392,10 @@ def run_ours(args):
                                           "occ_acc": round(float(mean_stats[2]), 2),
                                           "dist_acc": round(float(mean_stats[3]), 2)},
                        "scene_device_bytes": int(info.device_bytes),
+                       "counters": "timed renders request no per-ray MarchCounters (stats = NULL, "
+                                   "so K1 compiles the counter updates out); mean_ray_stats and the "
+                                   "algorithmic bytes come from an untimed render of the same "
+                                   "frames with counters (bit-identical images)",
                        "parallelism": f"dp{world} (camera sharding, NCCL gather to rank 0)"},
             "kernel_ms": {"march_K1": k1_avg, "shade_K2": k2_avg},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -706,6 +706,7 @@ __device__ __forceinline__ uint32_t probe_index(uint32_t x, uint32_t y, uint32_t
 // One marching point (march, occupancy.hpp:310-324): probe (:218-231) via the
 // per-level-1 probe code; occupied -> park for decode; empty -> next_step (:261-276).
 // Returns false when the ray left the clip interval.
+template <bool STATS>
 __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParams& p, Lane& s) {
     if (!(s.t < s.t1)) return false;
     float xu[3];
@@ -714,7 +715,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
         xu[a] = s.ray.o[a] + s.ray.d[a] * s.t;  // Ray::at (volume.hpp:19)
         s.xc[a] = fminf(fmaxf(xu[a], -1.0f), 1.0f);  // == clamp (common.hpp:94-97) for non-NaN
     }
-    ++s.n_march;
+    if constexpr (STATS) ++s.n_march;
     const int r0 = sc.occ_res[0], r1 = sc.occ_res[1];
     int i0[3];
 #pragma unroll
@@ -725,11 +726,11 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     const int e = int(code >> 8) & 7;
     // occupancy_probe counters: e + 1 levels read (5 when level 0 decides).
     // Written branch-free so every empty point reaches next_step on one path.
-    s.n_occ_acc += uint32_t(e) + 1u;
+    if constexpr (STATS) s.n_occ_acc += uint32_t(e) + 1u;
     // level-0 bit from the code's child byte (no second dependent load)
     const uint32_t child = uint32_t(i0[0] & 1) | (uint32_t(i0[1] & 1) << 1) | (uint32_t(i0[2] & 1) << 2);
     if (e == 4 && ((code >> child) & 1u)) {
-        ++s.n_occ;
+        if constexpr (STATS) ++s.n_occ;
         s.pending = true;
         return true;
     }
@@ -742,7 +743,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     uint32_t g = 0;
     const bool consult = p.use_grid && sc.dist && res < sc.dist_res;
     if (consult) {
-        ++s.n_dist;
+        if constexpr (STATS) ++s.n_dist;
         if (sc.dist_is_l1) {
             g = code & 0xffu;  // the probe code's own level-1 voxel (iu >> 1 == pidx's voxel)
         } else {
@@ -824,7 +825,8 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     return true;
 }
 
-template <int L, bool F16, bool MLPF, bool FC>
+// STATS = false (no per-ray counters requested): the counter updates are compiled out.
+template <int L, bool F16, bool MLPF, bool FC, bool STATS>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScene sc,
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
@@ -911,7 +913,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             // ---- step phase: cheap empty-space marching ----
 #pragma unroll 1
             for (int it = 0; it < p.step_burst; ++it) {
-                if (!march_point(sc, p, s)) {
+                if (!march_point<STATS>(sc, p, s)) {
                     write_result(p, s, true);
                     s.has_ray = false;
                     break;
@@ -950,26 +952,26 @@ __global__ void __launch_bounds__(256) raygen_kernel(const MarchParams p) {
     if (p.stats) p.stats[idx] = ngprt_ray_stats{0u, 0u, 0u, 0u};
 }
 
-template <int L, bool F16, bool MLPF, bool FC = false>
+template <int L, bool F16, bool MLPF, bool FC = false, bool STATS = true>
 int ctas_per_sm_t() {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<L, F16, MLPF, FC>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, march_kernel<L, F16, MLPF, FC, STATS>, kBlock, 0);
     return n > 0 ? n : 1;
 }
 
-template <int L, bool F16, bool MLPF, bool FC = false>
+template <int L, bool F16, bool MLPF, bool FC = false, bool STATS = true>
 void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
     static int grid = 0;
     if (!grid) {
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = sms * ctas_per_sm_t<L, F16, MLPF, FC>();
+        grid = sms * ctas_per_sm_t<L, F16, MLPF, FC, STATS>();
     }
     raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
     const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);
     const uint32_t need = (tiles + 3) / 4;  // 4 warps per CTA
-    march_kernel<L, F16, MLPF, FC><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
+    march_kernel<L, F16, MLPF, FC, STATS><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
 }
 
 template <int L>
@@ -979,7 +981,8 @@ void launch_l(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
         f16 ? launch_t<L, true, true>(sc, p, st) : launch_t<L, false, true>(sc, p, st);
     } else {
         if (f16 && sc.fast_decode && p.fast_color)
-            launch_t<L, true, false, true>(sc, p, st);
+            p.stats ? launch_t<L, true, false, true>(sc, p, st)
+                    : launch_t<L, true, false, true, false>(sc, p, st);
         else
             f16 ? launch_t<L, true, false>(sc, p, st) : launch_t<L, false, false>(sc, p, st);
     }
