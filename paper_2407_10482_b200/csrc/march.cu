@@ -2,19 +2,23 @@
 // of baked coarse rows and fine hash features, attention fusion and
 // front-to-back compositing with early stop.
 //
-// Execution model: persistent warps, one ray per lane. Rays come in 8x4 pixel
-// tiles from a global counter; a lane whose ray finishes is refilled from the
+// Execution model: persistent warps, one ray per lane. Rays come in 4x8 pixel
+// tiles (kRayTileW x kRayTileH) from a global counter; a lane whose ray finishes is refilled from the
 // warp's current tile. Lanes march independently, but a lane that reaches an
 // occupied point parks there until enough lanes of the warp are parked
 // (MarchParams::decode_min) or no lane can step: the expensive sample decode then runs
 // with most lanes converged instead of serialising against cheap empty steps.
 //
 // Parity: built with -fmad=false and every float/double operation is the
-// reference's, in its order. Two restructurings are
-// exact by construction and documented inline: (1) pyramid voxel indices at
+// reference's, in its order. Restructurings that are
+// exact by construction are documented inline: (1) pyramid voxel indices at
 // level k are the level-0 index >> k (power-of-two scaling commutes with
 // rounding), (2) division by a power-of-two resolution is multiplication by
-// its exact reciprocal. Reference citations are relative to
+// its exact reciprocal, (3) voxel_exit_step divides only for the axis with the
+// smallest exact ratio, (4) the unclamped point's voxel equals the clamped
+// point's. In tensor-MLP mode (FC) the colour-only channels use FMA and the
+// beta sigmoids a fast exp; everything that reaches density, transmittance,
+// early stop or the counters stays exact. Reference citations are relative to
 // /root/reference/proj/include/ngprt/.
 #include "render.cuh"
 
@@ -22,8 +26,8 @@ namespace ngprt_dev {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-// MarchParams::decode_min: parked lanes that trigger a warp-wide decode (default 12)
-// MarchParams::step_burst: marching points a stepping lane takes per round (default 4)
+// MarchParams::decode_min: parked lanes that trigger a warp-wide decode (default 6)
+// MarchParams::step_burst: marching points a stepping lane takes per round (default 6)
 #ifndef NGPRT_K1_MIN_BLOCKS
 #define NGPRT_K1_MIN_BLOCKS 5
 #endif

@@ -24,7 +24,7 @@ struct MarchParams {
     CamParams cams[kMaxCamsPerLaunch];
     int n_cams;
     uint32_t x0, y0, w, h;
-    uint32_t tiles_x, tiles_per_cam;  // 8x4 ray tiles over the window
+    uint32_t tiles_x, tiles_per_cam;  // kRayTileW x kRayTileH ray tiles over the window
     float step;
     int use_grid, max_step_rule, early_stop, keep_level;
     int decode_min, step_burst;  // K1 warp scheduling policy (tunable, see march.cu)
