@@ -21,7 +21,8 @@ for l in txt[start+1:]:
     if m and prev: continue
     prev=bool(m)
     if m:
-        cur=(m.group(1).split("/")[-1],int(m.group(2))); continue
+        chain=[(m.group(1).split("/")[-1],int(m.group(2)))]+[(a.split("/")[-1],int(b)) for a,b in re.findall(r'inlined at "([^"]+)", line (\d+)', m.group(3))]
+        cur=(chain[0][0],chain[0][1],tuple(chain)); continue
     m=re.match(r'\s*/\*([0-9a-f]{4,})\*/\s+(.*)',l)
     if m: insts.append((m.group(2).strip(),cur))
 csvtxt = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source=sass"],capture_output=True,text=True).stdout
@@ -43,8 +44,9 @@ iE=hdr.index("Instructions Executed");iT=hdr.index("Thread Instructions Executed
 print("rows",len(data),"sass",len(insts))
 by=collections.defaultdict(lambda:[0,0,0])
 for k in range(min(len(data),len(insts))):
-    key=insts[k][1] or ("?",0)
-    lab=f"{key[0]}:{key[1]}"
+    key=insts[k][1] or ("?",0,())
+    # label: innermost location, plus the call-site chain (outermost last)
+    lab=f"{key[0]}:{key[1]}" + ("|" + ">".join(f"{f}:{n}" for f,n in key[2][1:]) if len(key) > 2 and key[2][1:] else "")
     by[lab][0]+=int(data[k][iE] or 0);by[lab][1]+=int(data[k][iT] or 0);by[lab][2]+=int(data[k][iS] or 0)
 tot=[sum(v[i] for v in by.values()) for i in range(3)]
 print("warp inst %.3fG thread inst %.3fG"%(tot[0]/1e9,tot[1]/1e9))
