@@ -215,6 +215,23 @@ __device__ __forceinline__ float mac(bool fma, float acc, float w, float v) {
     return fma ? __fmaf_rn(w, v, acc) : acc + w * v;
 }
 
+// A pair of channels: with fma (both channels FMA-allowed) one sm_100 FFMA2
+// (packed f32x2; each half rounds exactly like a scalar FMA), else two mac()s.
+// Never used for exact channels: ptxas contracts packed multiply + add pairs.
+__device__ __forceinline__ void mac2(bool fma, float& a0, float& a1, float w, float v0, float v1) {
+    if (fma) {
+        unsigned long long acc, v, ww;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(v0), "f"(v1));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(ww), "l"(v));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+    } else {
+        a0 = mac(false, a0, w, v0);
+        a1 = mac(false, a1, w, v1);
+    }
+}
+
 // Coarse decoder channels that must stay exact: sigma_pre (0) and the omega
 // logits (8 + 2l), which set the density fuse weights of the variant modes.
 __device__ __forceinline__ constexpr bool exact_channel(int c) {
@@ -523,8 +540,12 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
             for (int i = 0; i < W / 2; ++i) {
                 const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&craw[k][i]));
-                dec[2 * i] = mac(FC && !exact_channel(2 * i), dec[2 * i], w[k], v.x);
-                dec[2 * i + 1] = mac(FC && !exact_channel(2 * i + 1), dec[2 * i + 1], w[k], v.y);
+                if (FC && !exact_channel(2 * i) && !exact_channel(2 * i + 1)) {
+                    mac2(true, dec[2 * i], dec[2 * i + 1], w[k], v.x, v.y);
+                } else {
+                    dec[2 * i] = mac(FC && !exact_channel(2 * i), dec[2 * i], w[k], v.x);
+                    dec[2 * i + 1] = mac(FC && !exact_channel(2 * i + 1), dec[2 * i + 1], w[k], v.y);
+                }
             }
     }
     // ---- attention (split_decoder_output, model.hpp:18-21) ----
@@ -577,8 +598,12 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float2 v = __half22float2(h[i]);
-                fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
-                fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
+                if (FC && i != 0) {
+                    mac2(true, fine[2 * i], fine[2 * i + 1], w[k], v.x, v.y);
+                } else {
+                    fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
+                    fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
+                }
             }
         }
         if (keep_level > 0 && l + 1 != keep_level) {
@@ -588,8 +613,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         float wo, wb;
         weights(l, wo, wb);
         out[0] += wo * fine[0];
+        out[1] = mac(FC, out[1], wb, fine[1]);
 #pragma unroll
-        for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
+        for (int c = 2; c < 8; c += 2) mac2(FC, out[c], out[c + 1], wb, fine[c], fine[c + 1]);
     }
     // ---- levels P..P+A-1 from shared memory ----
     if constexpr (A > 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -608,8 +634,12 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float2 v = __half22float2(h[i]);
-                fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
-                fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
+                if (FC && i != 0) {
+                    mac2(true, fine[2 * i], fine[2 * i + 1], w[k], v.x, v.y);
+                } else {
+                    fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
+                    fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
+                }
             }
         }
         if (keep_level > 0 && l + 1 != keep_level) {
@@ -619,8 +649,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         float wo, wb;
         weights(l, wo, wb);
         out[0] += wo * fine[0];
+        out[1] = mac(FC, out[1], wb, fine[1]);
 #pragma unroll
-        for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
+        for (int c = 2; c < 8; c += 2) mac2(FC, out[c], out[c + 1], wb, fine[c], fine[c + 1]);
     }
     // ---- remaining levels one round trip each ----
 #pragma unroll 1
@@ -634,8 +665,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         float wo, wb;
         weights(l, wo, wb);
         out[0] += wo * fine[0];
+        out[1] = mac(FC, out[1], wb, fine[1]);
 #pragma unroll
-        for (int c = 1; c < 8; ++c) out[c] = mac(FC, out[c], wb, fine[c]);
+        for (int c = 2; c < 8; c += 2) mac2(FC, out[c], out[c + 1], wb, fine[c], fine[c + 1]);
     }
 }
 
@@ -900,10 +932,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
                 const float sigma = activate_density(f[0], tab);
                 const float a = alpha_from_sigma(sigma, step, tab);
                 const float w = a * s.T;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) s.cd[c] = mac(FC, s.cd[c], w, f[1 + c]);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) s.fs[c] = mac(FC, s.fs[c], w, f[4 + c]);
+                s.cd[0] = mac(FC, s.cd[0], w, f[1]);
+                mac2(FC, s.cd[1], s.cd[2], w, f[2], f[3]);
+                mac2(FC, s.fs[0], s.fs[1], w, f[4], f[5]);
+                mac2(FC, s.fs[2], s.fs[3], w, f[6], f[7]);
                 s.T = s.T * (1.0f - a);
                 s.pending = false;
                 if (p.early_stop && s.T < float(2e-3)) {  // kEarlyStopTransmittance
