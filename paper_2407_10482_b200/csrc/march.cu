@@ -26,7 +26,7 @@ namespace ngprt_dev {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-// MarchParams::decode_min: parked lanes that trigger a warp-wide decode (default 6)
+// MarchParams::decode_min: parked lanes that trigger a warp-wide decode (default 4)
 // MarchParams::step_burst: marching points a stepping lane takes per round (default 6)
 #ifndef NGPRT_K1_MIN_BLOCKS
 #define NGPRT_K1_MIN_BLOCKS 5
@@ -463,7 +463,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
     // while in flight), issued together with the coarse and register-held rows
     constexpr int A = (L - P) < NGPRT_FINE_ASYNC_LEVELS ? (L - P) : NGPRT_FINE_ASYNC_LEVELS;
 #ifndef NGPRT_COARSE_FULL_ROW
-#define NGPRT_COARSE_FULL_ROW 0
+#define NGPRT_COARSE_FULL_ROW 1
 #endif
     // u32 words of a coarse row actually loaded (W <= 12: 128+64-bit loads, else one 256-bit)
     constexpr int CW = (W <= 12 && !NGPRT_COARSE_FULL_ROW) ? 6 : 8;
@@ -775,7 +775,9 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     // voxel_of clamps the index to [0, res-1], so the unclamped point's voxel is
     // the clamped point's: (x+1)*h < 0 <=> x < -1 and (x+1)*h >= res <=> x >= 1.
     const int* iu = i0;
-    const int res = sc.occ_res[exit_k];
+    // level resolution without a per-lane indexed constant load (divergent
+    // exit levels would serialise it): r_k = r0 >> k for a power-of-two r0
+    const int res = sc.occ_pow2 ? (r0 >> exit_k) : sc.occ_res[exit_k];
     uint32_t g = 0;
     const bool consult = p.use_grid && sc.dist && res < sc.dist_res;
     if (consult) {
@@ -814,7 +816,10 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
                 // lo = -1 + 2v/res and hi = lo + 2/res are exact for a power-of-two res
                 // (multiples of 2/res in [-1, 1]), so bound = -1 + (v + [d > 0]) * (2/res)
                 // is one exactly-rounded FMA with the same value
-                bound = __fmaf_rn(float(v + (d > 0.0f ? 1 : 0)), sc.lvl_two_over_res[exit_k], -1.0f);
+                // 2/r_k = (2/r0) * 2^k: exponent arithmetic on the (normal) power of two
+                const float two_over_res =
+                    __int_as_float(__float_as_int(sc.lvl_two_over_res[0]) + (exit_k << 23));
+                bound = __fmaf_rn(float(v + (d > 0.0f ? 1 : 0)), two_over_res, -1.0f);
             } else {
                 const float lo = -1.0f + (2.0f * float(v)) / float(res);
                 bound = d > 0.0f ? lo + sc.lvl_two_over_res[exit_k] : lo;

@@ -516,7 +516,7 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         // K1 scheduling policy; NGPRT_DECODE_MIN / NGPRT_STEP_BURST override for tuning
         static const int dmin = [] {
             const char* e = std::getenv("NGPRT_DECODE_MIN");
-            return e ? std::max(1, std::min(32, std::atoi(e))) : 6;
+            return e ? std::max(1, std::min(32, std::atoi(e))) : 4;
         }();
         static const int burst = [] {
             const char* e = std::getenv("NGPRT_STEP_BURST");
