@@ -871,7 +871,12 @@ template <int L, bool F16, bool MLPF, bool FC, bool STATS>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScene sc,
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
-    __shared__ float scratch[kBlock * (MLPF ? 8 * L : 8)];
+#ifndef NGPRT_SCRATCH_ROWS
+#define NGPRT_SCRATCH_ROWS (2 * L)
+#endif
+    // 2L attention logits per thread (8L fine features in MLP fusion). Keeping
+    // shared memory at 5 x 19.5 KB per SM leaves the 100 KB carve-out, so L1 keeps 156 KB.
+    __shared__ float scratch[kBlock * (MLPF ? 8 * L : NGPRT_SCRATCH_ROWS)];
     constexpr int kStageLv = (F16 && !MLPF)
         ? ((L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) < NGPRT_FINE_ASYNC_LEVELS
                ? (L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) : NGPRT_FINE_ASYNC_LEVELS)
