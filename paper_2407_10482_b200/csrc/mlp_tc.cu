@@ -14,7 +14,9 @@
 //      applies ReLU and writes the hidden row back to shared memory (split
 //      again) for layer 2;
 //   4. layer 3 (64 -> 3) runs on CUDA cores from TMEM, then
-//      rgb = sigmoid(C_d + out) with the glibc-expf sigmoid; rays with
+//      rgb = sigmoid(C_d + out) with the fast exp (the input already carries
+//      the tensor path's ~1e-6 error); biases, ReLU and layer 3 use the packed
+//      f32x2 FADD2 / FFMA2; rays with
 //      final_t == 1 stay black.
 #include <cuda_bf16.h>
 
@@ -125,6 +127,30 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
     for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// sm_100 packed f32x2 arithmetic (FADD2 / FFMA2): two IEEE f32 operations per
+// instruction (tensor mode only; its RGB tolerance covers the contraction).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long r) {
+    float2 f;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(r));
+    return f;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+    return upk2(d);
+}
+
 // Store one row of K values as bf16 hi/lo into the two canonical planes
 // (hardware round-to-nearest-even pair conversions, F2FP.BF16.F32.PACK_AB).
 template <int K>
@@ -137,7 +163,8 @@ __device__ __forceinline__ void store_row_split(uint8_t* hi, uint8_t* lo, int ro
             const float a = x[8 * c + 2 * j], b = x[8 * c + 2 * j + 1];
             const __nv_bfloat162 hb = __floats2bfloat162_rn(a, b);
             const float2 hf = __bfloat1622float2(hb);
-            const __nv_bfloat162 lb = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+            const float2 rem = add2(make_float2(a, b), make_float2(-hf.x, -hf.y));
+            const __nv_bfloat162 lb = __floats2bfloat162_rn(rem.x, rem.y);
             h[j] = *reinterpret_cast<const uint32_t*>(&hb);
             l[j] = *reinterpret_cast<const uint32_t*>(&lb);
         }
@@ -172,10 +199,8 @@ __global__ void __launch_bounds__(kThreads, 3)
     uint8_t* act_lo = act_hi + kActBytes;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(act_lo + kActBytes);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
-    __shared__ unsigned long long tab[32];
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    load_exp_table(tab);
     for (int i = tid; i < kImageBytes / 16; i += kThreads)
         reinterpret_cast<uint4*>(w_img)[i] = reinterpret_cast<const uint4*>(image)[i];
     const uint32_t s_mbar = uint32_t(__cvta_generic_to_shared(mbar));
@@ -199,7 +224,6 @@ __global__ void __launch_bounds__(kThreads, 3)
     // with the loops unrolled each is an FFMA/FADD operand, no shared-memory load
     const float* b0 = C.b0;
     const float* b1 = C.b1;
-    const float* w2 = C.w2;
     const float* b2 = C.b2;
     const uint32_t s_w = uint32_t(__cvta_generic_to_shared(w_img));
     const uint32_t s_ahi = uint32_t(__cvta_generic_to_shared(act_hi));
@@ -249,9 +273,10 @@ __global__ void __launch_bounds__(kThreads, 3)
         float h[kH];
         tmem_ld64(lane_base | d1, h);
 #pragma unroll
-        for (int i = 0; i < kH; ++i) {
-            const float v = h[i] + b0[i];
-            h[i] = v < 0.f ? 0.f : v;
+        for (int i = 0; i < kH; i += 2) {
+            const float2 v = add2(make_float2(h[i], h[i + 1]), make_float2(b0[i], b0[i + 1]));
+            h[i] = fmaxf(v.x, 0.f);
+            h[i + 1] = fmaxf(v.y, 0.f);
         }
         __syncwarp();
         store_row_split<kH>(act_hi, act_lo, tid, h);
@@ -268,22 +293,29 @@ __global__ void __launch_bounds__(kThreads, 3)
         asm volatile("tcgen05.fence::after_thread_sync;");
         // ---- layer 2 epilogue + layer 3 (64 -> 3) on CUDA cores ----
         tmem_ld64(lane_base | d2, h);
-        float y[3] = {b2[0], b2[1], b2[2]};
+        float2 y01 = make_float2(b2[0], b2[1]);
+        float y2 = b2[2];
 #pragma unroll
-        for (int i = 0; i < kH; ++i) {
-            float v = h[i] + b1[i];
-            v = v < 0.f ? 0.f : v;
-            y[0] = fmaf(w2[i], v, y[0]);
-            y[1] = fmaf(w2[64 + i], v, y[1]);
-            y[2] = fmaf(w2[128 + i], v, y[2]);
+        for (int i = 0; i < kH; i += 2) {
+            const float2 v = add2(make_float2(h[i], h[i + 1]), make_float2(b1[i], b1[i + 1]));
+            const float v0 = fmaxf(v.x, 0.f), v1 = fmaxf(v.y, 0.f);
+            y01 = fma2(make_float2(C.w2p[i][0], C.w2p[i][1]), make_float2(v0, v0), y01);
+            y2 = fmaf(C.w2c[i], v0, y2);
+            y01 = fma2(make_float2(C.w2p[i + 1][0], C.w2p[i + 1][1]), make_float2(v1, v1), y01);
+            y2 = fmaf(C.w2c[i + 1], v1, y2);
         }
+        const float y[3] = {y01.x, y01.y, y2};
         asm volatile("tcgen05.fence::before_thread_sync;");
         if (ray < n_rays) {
             float o[3] = {0.f, 0.f, 0.f};
             if (shade) {
-                o[0] = activate_sigmoid(r.a.x + y[0], tab);
-                o[1] = activate_sigmoid(r.a.y + y[1], tab);
-                o[2] = activate_sigmoid(r.a.z + y[2], tab);
+                // the sigmoid's input already carries the tensor path's ~1e-6
+                // error, so the fast exp / divide (~1e-7 relative) is used here
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float cd = c == 0 ? r.a.x : (c == 1 ? r.a.y : r.a.z);
+                    o[c] = __fdividef(1.0f, 1.0f + __expf(-(cd + y[c])));
+                }
             }
             rgb[3 * ray] = o[0];
             rgb[3 * ray + 1] = o[1];
@@ -331,7 +363,11 @@ void pack_psi_tc(const float* psi, void* out_v) {
 void shade_consts_from_psi(const float* psi, ShadeConsts* c) {
     std::memcpy(c->b0, psi + kPsiB0, 64 * 4);
     std::memcpy(c->b1, psi + kPsiB1, 64 * 4);
-    std::memcpy(c->w2, psi + kPsiW2, 192 * 4);
+    for (int i = 0; i < 64; ++i) {
+        c->w2p[i][0] = psi[kPsiW2 + i];
+        c->w2p[i][1] = psi[kPsiW2 + 64 + i];
+        c->w2c[i] = psi[kPsiW2 + 128 + i];
+    }
     std::memcpy(c->b2, psi + kPsiB2, 3 * 4);
     c->b2[3] = 0.f;
 }

@@ -43,9 +43,11 @@ void launch_probe_codes(const DevScene& sc, uint16_t* out, cudaStream_t st);
 // K2 (exact): f32 CUDA-core deferred MLP in the reference's operation order.
 void launch_shade_exact(const DevScene& sc, const RayAcc* acc, float* rgb, size_t n_rays,
                         cudaStream_t st);
-// psi's biases and 64 -> 3 layer, passed to K2 as a kernel parameter.
+// psi's biases and 64 -> 3 layer, passed to K2 as a kernel parameter. The
+// 64 -> 3 weights are stored as (W2[0][i], W2[1][i]) pairs (one FFMA2 operand)
+// followed by W2[2][i].
 struct ShadeConsts {
-    float b0[64], b1[64], w2[192], b2[4];
+    float b0[64], b1[64], w2p[64][2], w2c[64], b2[4];
 };
 void shade_consts_from_psi(const float* psi_host_packed, ShadeConsts* out);
 // K2 (tensor): tcgen05 deferred MLP, 128 rays per CTA tile.
