@@ -237,10 +237,18 @@ def run_ours(args):
     from paper_2407_10482_b200 import multigpu as mg
 
     rank, world, local = dist_env()
+    # Test hooks for the multi-rank flow on a 1-GPU box (functional only, the
+    # numbers mean nothing): NGPRT_BENCH_BACKEND=gloo, NGPRT_BENCH_SHARE_GPU=1.
+    backend = os.environ.get("NGPRT_BENCH_BACKEND", "nccl")
+    if os.environ.get("NGPRT_BENCH_SHARE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = scene_config(ng, args)
     W, H = cfg["width"], cfg["height"]
     synth = ng.SynthScene(**cfg)

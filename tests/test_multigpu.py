@@ -90,3 +90,27 @@ def test_sharding_covers_every_camera_and_tile_once():
         # weak scaling: over N steps each rank renders N distinct cameras
         for r in range(world):
             assert len({mg.camera_of(r, world, s, 64) for s in range(64 // world)}) == 64 // world
+
+
+@pytest.mark.gpu
+def test_bench_two_rank_flow_on_one_gpu():
+    """bench.py's multi-rank path (camera sharding, gather to rank 0, max-over-ranks
+    timing, one JSON line from rank 0) end to end with 2 ranks on one GPU over gloo.
+    Functional only: the driver's NCCL runs use one GPU per rank."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, NGPRT_BENCH_BACKEND="gloo", NGPRT_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(_free_port()), str(root / "bench.py"),
+                        "--gpus", "2", "--config", "c1_256", "--steps", "3", "--warmup", "3"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0
