@@ -3,59 +3,113 @@
 //   shade           volume.hpp:118-137  rgb = sigmoid(C_d + psi([C_d, F, sh(dir)]))
 //   TinyMlp::forward nn.hpp:175-196     acc = b[r]; acc += w[r][c] * a[c]; ReLU (hidden)
 //   black when final_t == 1             SPEC.md:326, training.hpp:321
-// Built with -fmad=false. One thread per ray; weights broadcast from shared memory.
+// Built with -fmad=false. Persistent CTAs, one thread per ray. The hidden
+// layers run input-major: for each input c, every output's accumulator takes
+// its c-th term, so each output still sums b, then c = 0, 1, ... in order. The
+// weights sit transposed in shared memory ([c][o], one broadcast LDS.128 per
+// four outputs) and the products of two outputs are one FMUL2 (sm_100 packed
+// f32x2 multiply, each half rounded like FMUL); the adds stay scalar FADDs
+// (ptxas contracts packed multiply + packed add into FFMA2, scalar adds it
+// leaves alone), so every operation rounds as the reference's.
 #include "render.cuh"
 
 namespace ngprt_dev {
 namespace {
 
 constexpr int kShadeBlock = 128;
+constexpr int kColsBytes = 64 * kShadeBlock * 4;
+
+// (a0, a1) += (w0 * x, w1 * x), each product and each sum rounded separately.
+__device__ __forceinline__ void mac_pair_exact(float& a0, float& a1, float w0, float w1, float x) {
+    unsigned long long wp, xp, p;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(wp) : "f"(w0), "f"(w1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(xp) : "f"(x));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(wp), "l"(xp));
+    float p0, p1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
+    a0 = __fadd_rn(a0, p0);
+    a1 = __fadd_rn(a1, p1);
+}
+
+// out[0..63] = b[0..63] + sum_c Wt[c][0..63] * in[c], c ascending. The inputs
+// come from this thread's shared-memory column (in[c * kShadeBlock]), so the c
+// loop stays rolled without spilling a register array to local memory.
+template <int K>
+__device__ __forceinline__ void dense64(const float* __restrict__ wt, const float* __restrict__ b,
+                                        const float* in, float* out) {
+#pragma unroll
+    for (int o = 0; o < 64; ++o) out[o] = b[o];
+#pragma unroll 1
+    for (int c = 0; c < K; ++c) {
+        const float x = in[c * kShadeBlock];
+        const float4* row = reinterpret_cast<const float4*>(wt + c * 64);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const float4 w = row[q];
+            mac_pair_exact(out[4 * q], out[4 * q + 1], w.x, w.y, x);
+            mac_pair_exact(out[4 * q + 2], out[4 * q + 3], w.z, w.w, x);
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kShadeBlock)
     shade_exact_kernel(const float* __restrict__ psi, const RayAcc* __restrict__ acc,
                        float* __restrict__ rgb, size_t n) {
-    __shared__ float w[kPsiTotal];
+    __shared__ __align__(16) float w0t[23 * 64];  // [c][o]
+    __shared__ __align__(16) float w1t[64 * 64];  // [c][o]
+    __shared__ float b0[64], b1[64], w2[3 * 64], b2[4];
+    extern __shared__ float cols[];  // 64 x kShadeBlock: per-thread layer inputs, column layout
     __shared__ unsigned long long tab[32];
     load_exp_table(tab);
-    for (int i = threadIdx.x; i < kPsiTotal; i += blockDim.x) w[i] = psi[i];
-    __syncthreads();
-    const size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    const RayAcc r = acc[i];
-    float out[3] = {0.f, 0.f, 0.f};
-    if (r.c.w != 0.f && r.a.w < 1.0f) {
-        float in[23];
-        in[0] = r.a.x; in[1] = r.a.y; in[2] = r.a.z;
-        in[3] = r.b.x; in[4] = r.b.y; in[5] = r.b.z; in[6] = r.b.w;
-        sh_encode(r.c.x, r.c.y, r.c.z, in + 7);
-        float h1[64];
-#pragma unroll 4
-        for (int o = 0; o < 64; ++o) {
-            float a = w[kPsiB0 + o];
-            const float* wr = w + kPsiW0 + o * 23;
-#pragma unroll
-            for (int c = 0; c < 23; ++c) a += wr[c] * in[c];
-            h1[o] = a < 0.0f ? 0.0f : a;
-        }
-        // Layer 2 row by row; layer 3 accumulates in the same c-order as the
-        // reference's inner loop, so h2 never needs to be materialised.
-        float y[3] = {w[kPsiB2], w[kPsiB2 + 1], w[kPsiB2 + 2]};
-        for (int o = 0; o < 64; ++o) {
-            float a = w[kPsiB1 + o];
-            const float* wr = w + kPsiW1 + o * 64;
-#pragma unroll
-            for (int c = 0; c < 64; ++c) a += wr[c] * h1[c];
-            const float h2 = a < 0.0f ? 0.0f : a;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) y[j] += w[kPsiW2 + j * 64 + o] * h2;
-        }
-        out[0] = activate_sigmoid(r.a.x + y[0], tab);
-        out[1] = activate_sigmoid(r.a.y + y[1], tab);
-        out[2] = activate_sigmoid(r.a.z + y[2], tab);
+    for (int i = threadIdx.x; i < 64 * 23; i += blockDim.x) {
+        const int o = i / 23, c = i % 23;
+        w0t[c * 64 + o] = psi[kPsiW0 + i];
     }
-    rgb[3 * i] = out[0];
-    rgb[3 * i + 1] = out[1];
-    rgb[3 * i + 2] = out[2];
+    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+        const int o = i / 64, c = i % 64;
+        w1t[c * 64 + o] = psi[kPsiW1 + i];
+    }
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+        b0[i] = psi[kPsiB0 + i];
+        b1[i] = psi[kPsiB1 + i];
+    }
+    for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) w2[i] = psi[kPsiW2 + i];
+    if (threadIdx.x < 3) b2[threadIdx.x] = psi[kPsiB2 + threadIdx.x];
+    __syncthreads();
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const RayAcc r = acc[i];
+        float out[3] = {0.f, 0.f, 0.f};
+        if (r.c.w != 0.f && r.a.w < 1.0f) {
+            float* col = cols + threadIdx.x;
+            const float f7[7] = {r.a.x, r.a.y, r.a.z, r.b.x, r.b.y, r.b.z, r.b.w};
+#pragma unroll
+            for (int c = 0; c < 7; ++c) col[c * kShadeBlock] = f7[c];
+            float sh[16];
+            sh_encode(r.c.x, r.c.y, r.c.z, sh);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) col[(7 + c) * kShadeBlock] = sh[c];
+            float h[64];
+            dense64<23>(w0t, b0, col, h);
+#pragma unroll
+            for (int o = 0; o < 64; ++o) col[o * kShadeBlock] = h[o] < 0.0f ? 0.0f : h[o];
+            float h2[64];
+            dense64<64>(w1t, b1, col, h2);
+            float y[3] = {b2[0], b2[1], b2[2]};
+#pragma unroll
+            for (int o = 0; o < 64; ++o) {
+                const float v = h2[o] < 0.0f ? 0.0f : h2[o];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) y[j] += w2[j * 64 + o] * v;
+            }
+            out[0] = activate_sigmoid(r.a.x + y[0], tab);
+            out[1] = activate_sigmoid(r.a.y + y[1], tab);
+            out[2] = activate_sigmoid(r.a.z + y[2], tab);
+        }
+        rgb[3 * i] = out[0];
+        rgb[3 * i + 1] = out[1];
+        rgb[3 * i + 2] = out[2];
+    }
 }
 
 }  // namespace
@@ -63,8 +117,20 @@ __global__ void __launch_bounds__(kShadeBlock)
 void launch_shade_exact(const DevScene& sc, const RayAcc* acc, float* rgb, size_t n_rays,
                         cudaStream_t st) {
     if (!n_rays) return;
-    const unsigned blocks = unsigned((n_rays + kShadeBlock - 1) / kShadeBlock);
-    shade_exact_kernel<<<blocks, kShadeBlock, 0, st>>>(sc.psi, acc, rgb, n_rays);
+    static int grid = 0;
+    if (!grid) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(shade_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kColsBytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shade_exact_kernel, kShadeBlock,
+                                                      kColsBytes);
+        grid = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    const size_t need = (n_rays + kShadeBlock - 1) / kShadeBlock;
+    const unsigned blocks = unsigned(need < size_t(grid) ? need : size_t(grid));
+    shade_exact_kernel<<<blocks, kShadeBlock, kColsBytes, st>>>(sc.psi, acc, rgb, n_rays);
 }
 
 }  // namespace ngprt_dev
