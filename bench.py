@@ -287,7 +287,7 @@ def run_ours(args):
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    k1_ms, k2_ms, launches, bytes_k1 = [], [], 0, 0.0
+    k0_ms, k1_ms, k2_ms, launches, bytes_k1 = [], [], [], 0, 0.0
     with Clocks(local) as clk:
         for i in range(args.steps):
             s = args.warmup + i
@@ -298,7 +298,8 @@ def run_ours(args):
             step_fn(s)
             ev[i][1].record(stream)
             torch.cuda.synchronize()
-            a, b, n = ng.render_timing(scene)
+            z, a, b, n = ng.render_timing3(scene)
+            k0_ms.append(z)
             k1_ms.append(a)
             k2_ms.append(b)
             launches += n
@@ -405,7 +406,8 @@ def run_ours(args):
                                    "algorithmic bytes come from an untimed render of the same "
                                    "frames with counters (bit-identical images)",
                        "parallelism": f"dp{world} (camera sharding, NCCL gather to rank 0)"},
-            "kernel_ms": {"march_K1": k1_avg, "shade_K2": k2_avg},
+            "kernel_ms": {"raygen_K0": sum(k0_ms) / len(k0_ms), "march_K1": k1_avg,
+                          "shade_K2": k2_avg},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "march_kernel (K1)",
                          "peak_source": peak_src,

@@ -175,10 +175,14 @@ ngprt_status ngprt_render_host_wait(const ngprt_scene* scene);
 
 /* Per-kernel device time of the most recent ngprt_render on this scene with
  * opts.profile set: CUDA events recorded on the render stream around the march
- * kernel (K1) and the deferred-MLP kernel (K2), summed over launches. Call
- * after synchronising that stream. Single-stream benchmarking aid. */
+ * kernel (K1) and the deferred-MLP kernel (K2), summed over launches; n_launches
+ * counts every kernel of the render (K0, K1, K2 per batch of up to 64 cameras).
+ * Call after synchronising that stream. Single-stream benchmarking aid. */
 ngprt_status ngprt_render_timing(const ngprt_scene* scene, float* ms_march, float* ms_shade,
                                  int* n_launches);
+/* The same with the ray-generation kernel (K0) timed separately. */
+ngprt_status ngprt_render_timing3(const ngprt_scene* scene, float* ms_raygen, float* ms_march,
+                                  float* ms_shade, int* n_launches);
 
 /* Occupancy structures on device (device pointers, async on stream).
  * levels_dev[k-1] receives level k (res base>>k), k = 1..4, u64 words x-fastest. */

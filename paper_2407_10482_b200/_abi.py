@@ -173,6 +173,8 @@ SIGNATURES = {
     "ngprt_render_host_wait": (C.c_int, [C.c_void_p]),
     "ngprt_render_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                       C.POINTER(C.c_int)]),
+    "ngprt_render_timing3": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                       C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "ngprt_build_pyramid": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p * (PYRAMID_LEVELS - 1),
                                       C.c_void_p]),
     "ngprt_build_distance_grid": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),

@@ -1006,7 +1006,7 @@ int ctas_per_sm_t() {
 }
 
 template <int L, bool F16, bool MLPF, bool FC = false, bool STATS = true>
-void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
+void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEvent_t between) {
     static int grid = 0;
     if (!grid) {
         int dev = 0, sms = 0;
@@ -1015,22 +1015,23 @@ void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
         grid = sms * ctas_per_sm_t<L, F16, MLPF, FC, STATS>();
     }
     raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
+    if (between) cudaEventRecord(between, st);
     const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);
     const uint32_t need = (tiles + 3) / 4;  // 4 warps per CTA
     march_kernel<L, F16, MLPF, FC, STATS><<<std::min<uint32_t>(grid, need), kBlock, 0, st>>>(sc, p);
 }
 
 template <int L>
-void launch_l(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
+void launch_l(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEvent_t ev) {
     const bool f16 = sc.storage == NGPRT_STORAGE_F16, mlp = sc.fusion == NGPRT_FUSION_MLP;
     if (mlp) {
-        f16 ? launch_t<L, true, true>(sc, p, st) : launch_t<L, false, true>(sc, p, st);
+        f16 ? launch_t<L, true, true>(sc, p, st, ev) : launch_t<L, false, true>(sc, p, st, ev);
     } else {
         if (f16 && sc.fast_decode && p.fast_color)
-            p.stats ? launch_t<L, true, false, true>(sc, p, st)
-                    : launch_t<L, true, false, true, false>(sc, p, st);
+            p.stats ? launch_t<L, true, false, true>(sc, p, st, ev)
+                    : launch_t<L, true, false, true, false>(sc, p, st, ev);
         else
-            f16 ? launch_t<L, true, false>(sc, p, st) : launch_t<L, false, false>(sc, p, st);
+            f16 ? launch_t<L, true, false>(sc, p, st, ev) : launch_t<L, false, false>(sc, p, st, ev);
     }
 }
 
@@ -1072,12 +1073,12 @@ __global__ void probe_code_kernel(const DevScene sc, uint16_t* __restrict__ out)
 
 }  // namespace
 
-void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st) {
+void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEvent_t between) {
     switch (sc.L) {
-        case 1: launch_l<1>(sc, p, st); break;
-        case 2: launch_l<2>(sc, p, st); break;
-        case 3: launch_l<3>(sc, p, st); break;
-        default: launch_l<4>(sc, p, st); break;
+        case 1: launch_l<1>(sc, p, st, between); break;
+        case 2: launch_l<2>(sc, p, st, between); break;
+        case 3: launch_l<3>(sc, p, st, between); break;
+        default: launch_l<4>(sc, p, st, between); break;
     }
 }
 

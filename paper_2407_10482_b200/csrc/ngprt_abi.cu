@@ -557,16 +557,16 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         p.stats = stats ? stats + size_t(c0) * per_cam : nullptr;
         const int li = s->prof_launches;
         NG_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned int), st));
-        if (o->profile) cudaEventRecord(s->prof_event(3 * li), st);
-        launch_march(s->ds, p, st);
-        if (o->profile) cudaEventRecord(s->prof_event(3 * li + 1), st);
+        if (o->profile) cudaEventRecord(s->prof_event(4 * li), st);
+        launch_march(s->ds, p, st, o->profile ? s->prof_event(4 * li + 1) : nullptr);
+        if (o->profile) cudaEventRecord(s->prof_event(4 * li + 2), st);
         float* out = rgb + size_t(c0) * per_cam * 3;
         if (o->mlp_mode == NGPRT_MLP_EXACT)
             launch_shade_exact(s->ds, acc, out, per_cam * nc, st);
         else
             launch_shade_tensor(s->ds, s->psi_tc, s->shade_consts, acc, out, per_cam * nc, st);
         if (o->profile) {
-            cudaEventRecord(s->prof_event(3 * li + 2), st);
+            cudaEventRecord(s->prof_event(4 * li + 3), st);
             s->prof_launches = li + 1;
         }
     }
@@ -756,22 +756,27 @@ ngprt_status ngprt_render_host_wait(const ngprt_scene* s) {
     return NGPRT_OK;
 }
 
-ngprt_status ngprt_render_timing(const ngprt_scene* s, float* ms_march, float* ms_shade,
-                                 int* n_launches) {
+ngprt_status ngprt_render_timing3(const ngprt_scene* s, float* ms_raygen, float* ms_march,
+                                  float* ms_shade, int* n_launches) {
     if (!s) return fail(NGPRT_EINVAL, "null scene");
     std::lock_guard<std::mutex> g(s->prof_mu);
-    float a = 0.f, b = 0.f;
-    for (int i = 0; i < s->prof_launches; ++i) {
-        float x = 0.f, y = 0.f;
-        NG_CUDA(cudaEventElapsedTime(&x, s->prof_events[3 * i], s->prof_events[3 * i + 1]));
-        NG_CUDA(cudaEventElapsedTime(&y, s->prof_events[3 * i + 1], s->prof_events[3 * i + 2]));
-        a += x;
-        b += y;
-    }
-    if (ms_march) *ms_march = a;
-    if (ms_shade) *ms_shade = b;
-    if (n_launches) *n_launches = 2 * s->prof_launches;
+    float t[3] = {0.f, 0.f, 0.f};
+    for (int i = 0; i < s->prof_launches; ++i)
+        for (int k = 0; k < 3; ++k) {
+            float x = 0.f;
+            NG_CUDA(cudaEventElapsedTime(&x, s->prof_events[4 * i + k], s->prof_events[4 * i + k + 1]));
+            t[k] += x;
+        }
+    if (ms_raygen) *ms_raygen = t[0];
+    if (ms_march) *ms_march = t[1];
+    if (ms_shade) *ms_shade = t[2];
+    if (n_launches) *n_launches = 3 * s->prof_launches;  // K0, K1, K2 per camera batch
     return NGPRT_OK;
+}
+
+ngprt_status ngprt_render_timing(const ngprt_scene* s, float* ms_march, float* ms_shade,
+                                 int* n_launches) {
+    return ngprt_render_timing3(s, nullptr, ms_march, ms_shade, n_launches);
 }
 
 ngprt_status ngprt_build_pyramid(const uint64_t* base, uint32_t base_res,

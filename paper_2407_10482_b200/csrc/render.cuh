@@ -37,7 +37,9 @@ struct MarchParams {
 
 // K1: march + gather + fuse + composite. Persistent warps, one ray per lane,
 // lanes refilled from a global tile counter.
-void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st);
+// K0 (ray generation) then K1; `between` (nullable) is recorded between the two.
+void launch_march(const DevScene& sc, const MarchParams& p, cudaStream_t st,
+                  cudaEvent_t between = nullptr);
 int march_ctas_per_sm(const DevScene& sc);
 void launch_probe_codes(const DevScene& sc, uint16_t* out, cudaStream_t st);
 // K2 (exact): f32 CUDA-core deferred MLP in the reference's operation order.

@@ -350,6 +350,15 @@ def render_timing(scene: Scene):
     return a.value, b.value, n.value
 
 
+def render_timing3(scene: Scene):
+    """(ms in K0 raygen, ms in K1 march, ms in K2 shade, kernel launches) of the last
+    profiled render."""
+    z, a, b, n = C.c_float(), C.c_float(), C.c_float(), C.c_int()
+    check(lib().ngprt_render_timing3(scene.handle, C.byref(z), C.byref(a), C.byref(b), C.byref(n)),
+          "ngprt_render_timing3")
+    return z.value, a.value, b.value, n.value
+
+
 def render_host(scene: Scene, cams, opts: Opts | None = None, out=None, stats=None):
     """Host-buffer render (ngprt_render_host): copies cameras in and RGB out."""
     opts = opts or Opts()
