@@ -37,15 +37,21 @@ def tile_windows(width: int, height: int, tile: int, rank: int, world: int):
     return out
 
 
-def gather_frames(frame: torch.Tensor, world: int, dst: int = 0):
+def gather_frames(frame: torch.Tensor, world: int, dst: int = 0, bufs=None,
+                  async_op: bool = False):
     """Gather one equally-shaped frame per rank to `dst` (NCCL gather). Returns the
-    list of frames on dst, None elsewhere."""
+    list of frames on dst, None elsewhere; with async_op, (list, work) where
+    work.wait() orders the caller's current stream after the transfer (NCCL) so a
+    render enqueued before the wait overlaps the gather of an earlier frame."""
     if world == 1:
-        return [frame]
+        return ([frame], None) if async_op else [frame]
     rank = dist.get_rank()
-    bufs = [torch.empty_like(frame) for _ in range(world)] if rank == dst else None
-    dist.gather(frame, gather_list=bufs, dst=dst)
-    return bufs
+    if rank == dst and bufs is None:
+        bufs = [torch.empty_like(frame) for _ in range(world)]
+    work = dist.gather(frame, gather_list=bufs if rank == dst else None, dst=dst,
+                       async_op=async_op)
+    out = bufs if rank == dst else None
+    return (out, work) if async_op else out
 
 
 def assemble_tiles(tiles_by_rank, width: int, height: int, tile: int, world: int,
