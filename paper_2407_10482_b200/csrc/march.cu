@@ -28,10 +28,14 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 // MarchParams::decode_min: parked lanes that trigger a warp-wide decode (default 4)
 // MarchParams::step_burst: marching points a stepping lane takes per round (default 6)
-#ifndef NGPRT_K1_MIN_BLOCKS
-#define NGPRT_K1_MIN_BLOCKS 5
+// CTAs per SM the register allocation targets: 6 (80 registers, 24 warps) for
+// L <= 2, 5 (96 registers) for L = 3, 4, whose wider decode would spill at 80.
+// NGPRT_K1_MIN_BLOCKS overrides both.
+#ifdef NGPRT_K1_MIN_BLOCKS
+template <int L> constexpr int kMinBlocks = NGPRT_K1_MIN_BLOCKS;
+#else
+template <int L> constexpr int kMinBlocks = L <= 2 ? 6 : 5;
 #endif
-constexpr int kMinBlocks = NGPRT_K1_MIN_BLOCKS;  // 5: 65536 / (128 * 5) = 102 regs
 
 struct Ray {
     float o[3], d[3];
@@ -671,6 +675,17 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
     }
 }
 
+// NGPRT_LANE_SMEM: a lane's parked sample position and colour accumulators
+// (C_d, F) live in its shared-memory scratch column instead of registers (they
+// are touched once per sample), which frees ~10 registers for the decode.
+#ifndef NGPRT_LANE_SMEM
+#define NGPRT_LANE_SMEM 1
+#endif
+constexpr bool kLaneSmem = NGPRT_LANE_SMEM != 0;
+constexpr int kLaneRows = kLaneSmem ? 10 : 0;  // xc[3], cd[3], fs[4]
+// Scratch-column row of lane field j (0..9) after `base` attention rows.
+__device__ __forceinline__ float& lane_row(float* scr, int base, int j) { return scr[(base + j) * kBlock]; }
+
 // Per-lane ray state.
 struct Lane {
     Ray ray;
@@ -682,10 +697,17 @@ struct Lane {
     bool has_ray, pending;
 };
 
-__device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s, bool valid) {
+__device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s, bool valid,
+                                             float* scr, int lb) {
     RayAcc r;
-    r.a = make_float4(s.cd[0], s.cd[1], s.cd[2], s.T);
-    r.b = make_float4(s.fs[0], s.fs[1], s.fs[2], s.fs[3]);
+    if constexpr (kLaneSmem) {
+        r.a = make_float4(lane_row(scr, lb, 3), lane_row(scr, lb, 4), lane_row(scr, lb, 5), s.T);
+        r.b = make_float4(lane_row(scr, lb, 6), lane_row(scr, lb, 7), lane_row(scr, lb, 8),
+                          lane_row(scr, lb, 9));
+    } else {
+        r.a = make_float4(s.cd[0], s.cd[1], s.cd[2], s.T);
+        r.b = make_float4(s.fs[0], s.fs[1], s.fs[2], s.fs[3]);
+    }
     r.c = make_float4(valid ? s.ray.d[0] : 0.f, valid ? s.ray.d[1] : 0.f,
                       valid ? s.ray.d[2] : 0.f, valid ? 1.f : 0.f);
     p.acc[s.out_idx] = r;
@@ -702,7 +724,7 @@ __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s
 // Start the ray of slot `slot` (0..31) of ray tile `tile` from the K0 ray
 // buffer. Rays K0 already finished (missed the ROI) leave the lane idle.
 __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, uint32_t slot,
-                                          Lane& s) {
+                                          Lane& s, float* scr, int lb) {
     const uint32_t cam = tile / p.tiles_per_cam, tt = tile % p.tiles_per_cam;
     const uint32_t px = (tt % p.tiles_x) * kRayTileW + (slot % kRayTileW),
                    py = (tt / p.tiles_x) * kRayTileH + (slot / kRayTileW);
@@ -716,8 +738,13 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
     s.ray.d[0] = b.x; s.ray.d[1] = b.y; s.ray.d[2] = b.z;
     s.t = a.w;
     s.t1 = b.w;
-    s.cd[0] = s.cd[1] = s.cd[2] = 0.f;
-    s.fs[0] = s.fs[1] = s.fs[2] = s.fs[3] = 0.f;
+    if constexpr (kLaneSmem) {
+#pragma unroll
+        for (int j = 3; j < 10; ++j) lane_row(scr, lb, j) = 0.f;
+    } else {
+        s.cd[0] = s.cd[1] = s.cd[2] = 0.f;
+        s.fs[0] = s.fs[1] = s.fs[2] = s.fs[3] = 0.f;
+    }
     s.T = 1.0f;
     s.n_march = s.n_occ = s.n_occ_acc = s.n_dist = 0;
     s.pending = false;
@@ -743,19 +770,20 @@ __device__ __forceinline__ uint32_t probe_index(uint32_t x, uint32_t y, uint32_t
 // per-level-1 probe code; occupied -> park for decode; empty -> next_step (:261-276).
 // Returns false when the ray left the clip interval.
 template <bool STATS>
-__device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParams& p, Lane& s) {
+__device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParams& p, Lane& s,
+                                            float* scr, int lb) {
     if (!(s.t < s.t1)) return false;
-    float xu[3];
+    float xu[3], xc[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         xu[a] = s.ray.o[a] + s.ray.d[a] * s.t;  // Ray::at (volume.hpp:19)
-        s.xc[a] = fminf(fmaxf(xu[a], -1.0f), 1.0f);  // == clamp (common.hpp:94-97) for non-NaN
+        xc[a] = fminf(fmaxf(xu[a], -1.0f), 1.0f);  // == clamp (common.hpp:94-97) for non-NaN
     }
     if constexpr (STATS) ++s.n_march;
     const int r0 = sc.occ_res[0], r1 = sc.occ_res[1];
     int i0[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) i0[a] = voxel_1d_clamped(s.xc[a], sc.occ_h0, r0);
+    for (int a = 0; a < 3; ++a) i0[a] = voxel_1d_clamped(xc[a], sc.occ_h0, r0);
     // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
     const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
     const uint32_t code = __ldg(sc.probe + pidx);
@@ -768,6 +796,11 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     if (e == 4 && ((code >> child) & 1u)) {
         if constexpr (STATS) ++s.n_occ;
         s.pending = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if constexpr (kLaneSmem) lane_row(scr, lb, a) = xc[a];
+            else s.xc[a] = xc[a];
+        }
         return true;
     }
     const int exit_k = e == 4 ? 0 : 4 - e;
@@ -786,9 +819,9 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
             g = code & 0xffu;  // the probe code's own level-1 voxel (iu >> 1 == pidx's voxel)
         } else {
             const int gr = sc.dist_res;
-            const int vx = voxel_1d_clamped(s.xc[0], sc.dist_h, gr),
-                      vy = voxel_1d_clamped(s.xc[1], sc.dist_h, gr),
-                      vz = voxel_1d_clamped(s.xc[2], sc.dist_h, gr);
+            const int vx = voxel_1d_clamped(xc[0], sc.dist_h, gr),
+                      vy = voxel_1d_clamped(xc[1], sc.dist_h, gr),
+                      vz = voxel_1d_clamped(xc[2], sc.dist_h, gr);
             g = __ldg(sc.dist + (size_t(vx) + size_t(gr) * (size_t(vy) + size_t(gr) * vz)));
         }
     }
@@ -868,7 +901,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
 
 // STATS = false (no per-ray counters requested): the counter updates are compiled out.
 template <int L, bool F16, bool MLPF, bool FC, bool STATS>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScene sc,
+__global__ void __launch_bounds__(kBlock, kMinBlocks<L>) march_kernel(const DevScene sc,
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
 #ifndef NGPRT_SCRATCH_ROWS
@@ -876,7 +909,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
 #endif
     // 2L attention logits per thread (8L fine features in MLP fusion). Keeping
     // shared memory at 5 x 19.5 KB per SM leaves the 100 KB carve-out, so L1 keeps 156 KB.
-    __shared__ float scratch[kBlock * (MLPF ? 8 * L : NGPRT_SCRATCH_ROWS)];
+    constexpr int kAttRows = MLPF ? 8 * L : NGPRT_SCRATCH_ROWS;
+    __shared__ float scratch[kBlock * (kAttRows + kLaneRows)];
+    constexpr int lb = kAttRows;  // first lane-state row
     constexpr int kStageLv = (F16 && !MLPF)
         ? ((L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) < NGPRT_FINE_ASYNC_LEVELS
                ? (L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) : NGPRT_FINE_ASYNC_LEVELS)
@@ -915,7 +950,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             const uint32_t avail = 32u - tile_next_slot;
             const uint32_t take = min(uint32_t(__popc(need)), avail);
             const uint32_t rank = __popc(need & lt_mask);
-            if (((need >> lane) & 1u) && rank < take) start_ray(p, tile, tile_next_slot + rank, s);
+            if (((need >> lane) & 1u) && rank < take) start_ray(p, tile, tile_next_slot + rank, s, scr, lb);
             tile_next_slot += take;
             need = __ballot_sync(kFull, !s.has_ray);
         }
@@ -930,26 +965,41 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             // ---- decode phase: emit(t) of the canonical render_ray ----
             if (s.has_ray && s.pending) {
                 float f[8];
+                float xq[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) xq[a] = kLaneSmem ? lane_row(scr, lb, a) : s.xc[a];
                 if constexpr (F16 && !MLPF) {
                     if (sc.fast_decode)
-                        decode_point_fast<L, FC>(sc, s.xc, p.keep_level, tab, scr, stage, f);
+                        decode_point_fast<L, FC>(sc, xq, p.keep_level, tab, scr, stage, f);
                     else
-                        decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
+                        decode_point<L, F16, MLPF>(sc, xq, p.keep_level, tab, scr, f);
                 } else {
-                    decode_point<L, F16, MLPF>(sc, s.xc, p.keep_level, tab, scr, f);
+                    decode_point<L, F16, MLPF>(sc, xq, p.keep_level, tab, scr, f);
                 }
                 // composite, volume.hpp:61-70
                 const float sigma = activate_density(f[0], tab);
                 const float a = alpha_from_sigma(sigma, step, tab);
                 const float w = a * s.T;
-                s.cd[0] = mac(FC, s.cd[0], w, f[1]);
-                mac2(FC, s.cd[1], s.cd[2], w, f[2], f[3]);
-                mac2(FC, s.fs[0], s.fs[1], w, f[4], f[5]);
-                mac2(FC, s.fs[2], s.fs[3], w, f[6], f[7]);
+                if constexpr (kLaneSmem) {
+                    float c[7];
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) c[j] = lane_row(scr, lb, 3 + j);
+                    c[0] = mac(FC, c[0], w, f[1]);
+                    mac2(FC, c[1], c[2], w, f[2], f[3]);
+                    mac2(FC, c[3], c[4], w, f[4], f[5]);
+                    mac2(FC, c[5], c[6], w, f[6], f[7]);
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) lane_row(scr, lb, 3 + j) = c[j];
+                } else {
+                    s.cd[0] = mac(FC, s.cd[0], w, f[1]);
+                    mac2(FC, s.cd[1], s.cd[2], w, f[2], f[3]);
+                    mac2(FC, s.fs[0], s.fs[1], w, f[4], f[5]);
+                    mac2(FC, s.fs[2], s.fs[3], w, f[6], f[7]);
+                }
                 s.T = s.T * (1.0f - a);
                 s.pending = false;
                 if (p.early_stop && s.T < float(2e-3)) {  // kEarlyStopTransmittance
-                    write_result(p, s, true);
+                    write_result(p, s, true, scr, lb);
                     s.has_ray = false;
                 } else {
                     s.t += step;
@@ -959,8 +1009,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) march_kernel(const DevScen
             // ---- step phase: cheap empty-space marching ----
 #pragma unroll 1
             for (int it = 0; it < p.step_burst; ++it) {
-                if (!march_point<STATS>(sc, p, s)) {
-                    write_result(p, s, true);
+                if (!march_point<STATS>(sc, p, s, scr, lb)) {
+                    write_result(p, s, true, scr, lb);
                     s.has_ray = false;
                     break;
                 }
