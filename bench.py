@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--config", default="c3_1080p")
     ap.add_argument("--mlp", choices=["tensor", "exact"], default=os.environ.get("NGPRT_MLP", "tensor"))
     ap.add_argument("--no-l2-flush", action="store_true")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="cameras per ngprt_render call (one step renders a batch of frames)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target wall time of the bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -194,6 +196,7 @@ def run_reference(args):
     cfg = scene_config(ng, args)
     W, H = cfg["width"], cfg["height"]
     scene = ng.SynthScene(**cfg)
+    UNIT = f"fps ({W}x{H} frames/s, all GPUs)"
     cams = ng.cameras(N_CAMS, W, H)
     sys.path.insert(0, str(ROOT / "tests"))
     from checkers import REF_SO, CpuScene
@@ -254,16 +257,24 @@ def run_ours(args):
     synth = ng.SynthScene(**cfg)
     scene = ng.Scene(synth, device=local)
     info = scene.info()
-    cams = ng.cameras(N_CAMS, W, H)
+    # the config's camera ring (c2: the 100-camera orbit), at least 64 distinct views
+    n_cams = max(N_CAMS, int(cfg.get("n_cams", 1)))
+    B = max(1, args.batch)
+    cams = ng.cameras(n_cams, W, H)
     opts = ng.Opts(mlp=args.mlp, profile=True)
+    UNIT = f"fps ({W}x{H} frames/s, all GPUs)"
     stream = torch.cuda.current_stream(dev)
     # two frame buffers: step s renders frame s while frame s-1 is gathered to rank 0
-    outs = [torch.empty((1, H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+    outs = [torch.empty((B, H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
     gbufs = [torch.empty_like(outs[0]) for _ in range(world)] if rank == 0 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def cam_of(step):
-        return cams[mg.camera_of(rank, world, step, N_CAMS)]
+    def cam_ids(step):
+        """This rank's cameras of step `step` (B consecutive frames of its share)."""
+        return [mg.camera_of(rank, world, step * B + j, n_cams) for j in range(B)]
+
+    def cams_of(step):
+        return [cams[c] for c in cam_ids(step)]
 
     def step_fn(step, last=False):
         out = outs[step & 1]
@@ -272,7 +283,7 @@ def run_ours(args):
             # NCCL gather of the previous frame, overlapping this frame's render
             # (the NCCL stream waits for the work already on `stream`: frame step-1)
             _, work = mg.gather_frames(outs[(step - 1) & 1], world, bufs=gbufs, async_op=True)
-        ng.render(scene, [cam_of(step)], opts, out=out, stream=stream)
+        ng.render(scene, cams_of(step), opts, out=out, stream=stream)
         if work is not None:
             work.wait()  # the step ends after the transfer
         if world > 1 and last:
@@ -281,8 +292,7 @@ def run_ours(args):
     # per-camera algorithmic bytes from the bit-exact counters (untimed)
     b_store = 2 if info.storage == 2 else 4
     alg = {}
-    for s in range(args.warmup + args.steps):
-        c = mg.camera_of(rank, world, s, N_CAMS)
+    for c in sorted({c for s in range(args.warmup + args.steps) for c in cam_ids(s)}):
         if c not in alg:
             rgb_c, st = ng.render(scene, [cams[c]], ng.Opts(mlp=args.mlp), stats=True)
             st = st.cpu().numpy()
@@ -313,13 +323,13 @@ def run_ours(args):
             k1_ms.append(a)
             k2_ms.append(b)
             launches += n
-            bytes_k1 += alg[mg.camera_of(rank, world, s, N_CAMS)][0]
+            bytes_k1 += sum(alg[c][0] for c in cam_ids(s))
     total_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    frames = args.steps * world
+    frames = args.steps * world * B
     fps = frames / (total_ms / 1e3)
 
     # ---- e2e through the host-buffer C ABI (H2D camera, D2H RGB inside) ----
@@ -332,18 +342,18 @@ def run_ours(args):
     # (b) the synchronous call ngprt_render_host per frame (L2 flushed before
     #     each), reported as e2e_sync.
     opts_e2e = ng.Opts(mlp=args.mlp)
-    host_bufs = [torch.empty((1, H, W, 3), dtype=torch.float32).pin_memory().numpy()
+    host_bufs = [torch.empty((B, H, W, 3), dtype=torch.float32).pin_memory().numpy()
                  for _ in range(2)]
     for s in range(min(2, args.warmup)):
-        ng.render_host(scene, [cam_of(s)], opts_e2e, out=host_bufs[0])
-        ng.render_host_async(scene, [cam_of(s)], host_bufs[s & 1], opts_e2e)
+        ng.render_host(scene, cams_of(s), opts_e2e, out=host_bufs[0])
+        ng.render_host_async(scene, cams_of(s), host_bufs[s & 1], opts_e2e)
     ng.render_host_wait(scene)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for i in range(args.steps):
-        ng.render_host_async(scene, [cam_of(args.warmup + i)], host_bufs[i & 1], opts_e2e)
+        ng.render_host_async(scene, cams_of(args.warmup + i), host_bufs[i & 1], opts_e2e)
     ng.render_host_wait(scene)
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -357,7 +367,7 @@ def run_ours(args):
             flush.fill_(i & 0xFF)
             torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ng.render_host(scene, [cam_of(args.warmup + i)], opts_e2e, out=host_bufs[0])
+        ng.render_host(scene, cams_of(args.warmup + i), opts_e2e, out=host_bufs[0])
         e2e_sync_s += time.perf_counter() - t0
     t = torch.tensor([e2e_sync_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -384,12 +394,12 @@ def run_ours(args):
                         for k in ("l2_read_gbs", "l2_gather32_gbs", "l2_gather16_gbs",
                                   "hbm_gather32_gbs") if k in pj}
             ceilings["source"] = f"profiles/{pk[-1].name} ({pj.get('method', '')})"
-        shaded = np.mean([alg[mg.camera_of(rank, world, args.warmup + i, N_CAMS)][2]
+        shaded = np.mean([sum(alg[c][2] for c in cam_ids(args.warmup + i))
                           for i in range(args.steps)])
         k2_avg = sum(k2_ms) / len(k2_ms)
         k2_flop = 11520.0 * shaded  # 11,520 FLOP per shaded ray
-        mean_stats = np.mean([alg[mg.camera_of(rank, world, args.warmup + i, N_CAMS)][1]
-                              for i in range(args.steps)], axis=0)
+        mean_stats = np.mean([alg[c][1] for i in range(args.steps)
+                              for c in cam_ids(args.warmup + i)], axis=0)
         line = {
             "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -403,7 +413,9 @@ def run_ours(args):
                 f"L_C={cfg['L_C']}, {cfg['occ_base_res']}^3 pyramid, "
                 f"{int(synth.desc.dist_res)}^3 distance grid, occupancy "
                 f"{100 * synth.occupancy_fraction():.2f}%, mlp={args.mlp}"),
-                       "cameras": f"sphere_views({N_CAMS}, 2.9); rank r renders (r + N*step) % {N_CAMS}",
+                       "cameras": f"sphere_views({n_cams}, 2.9); rank r renders cameras "
+                                  f"(r + N*(step*{B} + j)) % {n_cams}, j < {B} per step"
+                                  + (f" (one ngprt_render call of {B} cameras)" if B > 1 else ""),
                        "l2": "flushed (256 MiB write) before every timed step" if not args.no_l2_flush
                              else "not flushed; scene (4.4 GB) larger than L2",
                        "mean_ray_stats": {"marching": round(float(mean_stats[0]), 2),
@@ -433,9 +445,9 @@ def run_ours(args):
                                   "per FLOP (hi/lo split) and runs layer 3 on CUDA cores"},
             "e2e_sync": {"value": e2e_sync_fps, "unit": UNIT,
                          "api": "ngprt_render_host per frame (pinned host RGB, L2 flushed before each)"},
-            "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 168,
-                    "d2h_bytes_per_step": W * H * 12,
-                    "ms_per_step": 1e3 * frames / e2e_fps / max(world, 1),
+            "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 168 * B,
+                    "d2h_bytes_per_step": B * W * H * 12,
+                    "ms_per_step": 1e3 * frames / e2e_fps / args.steps,
                     "timer": "host wall clock from the first enqueue to ngprt_render_host_wait "
                              "returning (every frame's RGB is in pinned host memory); close to the "
                              "device value because each 24.9 MB copy runs on the copy engine while "
@@ -448,7 +460,7 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_sample(synth, cam_of(0), W, H, args.cpu_seconds)
+            cb = cpu_sample(synth, cams_of(0)[0], W, H, args.cpu_seconds)
             line["cpu_baseline"] = {"value": cb["fps"], "unit": UNIT, "cores": cb["cores"],
                                     "kind": cb["kind"], "sample": cb["sample"],
                                     "mrays_per_s": cb["mrays_per_s"],

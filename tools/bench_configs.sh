@@ -4,9 +4,11 @@ out=gpurun_out/configs_$tag.jsonl; : > $out
 run() { timeout 600 python bench.py --steps ${STEPS:-8} --warmup 3 --no-cpu-baseline "$@" 2>/dev/null | tail -1 >> $out; }
 run --config c1_256
 run --config c2_blob800
+run --config c2_blob800 --batch 50
 run --config c3_1080p
 run --config c3_1080p --mlp exact
 run --config c4_1080p_x64
+run --config c4_1080p_x64 --batch 64
 for nb in 10 35 140 560 2240; do run --config c5_2160p --scene n_boxes=$nb; done
 python - <<'PY' $out
 import json,sys

@@ -21,9 +21,11 @@ ROOT = Path(__file__).resolve().parents[1]
 OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
 CONFIG_NAMES = ["c1_256 (256x256, L=4, 2^19, bench, 256^3/128^3 DT)",
-                "c2_blob800 (800x800, L=2, 2^22, blob)",
+                "c2_blob800 (800x800, L=2, 2^22, blob), one frame per call",
+                "c2_blob800, 100-camera orbit as 2 calls of 50 cameras",
                 "c3_1080p (1920x1080, L=2, 2^21, mip360)", "c3_1080p, exact CUDA-core MLP",
-                "c4_1080p_x64 (per-frame, camera ring)"] + \
+                "c4_1080p_x64 (per-frame, camera ring)",
+                "c4_1080p_x64, 64 cameras per call"] + \
                [f"c5_2160p boxes={n} (3840x2160, L=2, 2^22)" for n in (10, 35, 140, 560, 2240)]
 
 
