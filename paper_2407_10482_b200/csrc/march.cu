@@ -448,24 +448,32 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
 
 // Fast-path decode (fp16 storage, power-of-two hashed fine levels, 32-bit
 // coarse keys): the coarse rows and the rows of the first P fine levels are
-// requested before any of them is consumed, so a sample costs one dependent
-// gather round trip instead of 1 + L. Arithmetic and its order are exactly
-// decode_point's (same per-corner accumulation, same in-order fuse).
+// requested before any of them is consumed (one dependent gather round trip for
+// them); the next A levels are requested with them too but land in shared
+// memory (cp.async, no registers held); any further level is one round trip
+// each. Arithmetic and its order are exactly decode_point's (same per-corner
+// accumulation, same in-order fuse). At L <= 2 (6 CTAs per SM) level 1 takes
+// its own round trip (A = 0): the 16 KB staging buffer per CTA costs more L1
+// than the extra trip costs latency; at L = 3, 4 (5 CTAs) one level is staged.
 #ifndef NGPRT_FINE_PREFETCH
 #define NGPRT_FINE_PREFETCH 1
 #endif
-#ifndef NGPRT_FINE_ASYNC_LEVELS
-#define NGPRT_FINE_ASYNC_LEVELS 1
+template <int L> constexpr int kFineP = NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L;
+#ifdef NGPRT_FINE_ASYNC_LEVELS
+template <int L> constexpr int kFineAsync = NGPRT_FINE_ASYNC_LEVELS;
+#else
+template <int L> constexpr int kFineAsync = L <= 2 ? 0 : 1;
 #endif
+template <int L> constexpr int kFineA = (L - kFineP<L>) < kFineAsync<L> ? (L - kFineP<L>) : kFineAsync<L>;
 template <int L, bool FC>
 __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const float x[3],
                                                   int keep_level, const unsigned long long* tab,
                                                   float* scr, uint4* stage, float out[8]) {
     constexpr int W = 8 + 2 * L;
-    constexpr int P = NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L;
+    constexpr int P = kFineP<L>;
     // fine levels P .. P+A-1 go to shared memory with cp.async (no registers held
     // while in flight), issued together with the coarse and register-held rows
-    constexpr int A = (L - P) < NGPRT_FINE_ASYNC_LEVELS ? (L - P) : NGPRT_FINE_ASYNC_LEVELS;
+    constexpr int A = kFineA<L>;
 #ifndef NGPRT_COARSE_FULL_ROW
 #define NGPRT_COARSE_FULL_ROW 1
 #endif
@@ -907,15 +915,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks<L>) march_kernel(const DevS
 #ifndef NGPRT_SCRATCH_ROWS
 #define NGPRT_SCRATCH_ROWS (2 * L)
 #endif
-    // 2L attention logits per thread (8L fine features in MLP fusion). Keeping
-    // shared memory at 5 x 19.5 KB per SM leaves the 100 KB carve-out, so L1 keeps 156 KB.
+    // 2L attention logits per thread (8L fine features in MLP fusion), then the
+    // lane-state rows.
     constexpr int kAttRows = MLPF ? 8 * L : NGPRT_SCRATCH_ROWS;
     __shared__ float scratch[kBlock * (kAttRows + kLaneRows)];
     constexpr int lb = kAttRows;  // first lane-state row
-    constexpr int kStageLv = (F16 && !MLPF)
-        ? ((L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) < NGPRT_FINE_ASYNC_LEVELS
-               ? (L - (NGPRT_FINE_PREFETCH < L ? NGPRT_FINE_PREFETCH : L)) : NGPRT_FINE_ASYNC_LEVELS)
-        : 0;
+    constexpr int kStageLv = (F16 && !MLPF) ? kFineA<L> : 0;
     __shared__ uint4 fstage[kStageLv > 0 ? kStageLv * 8 * kBlock : 1];  // cp.async fine rows
     load_exp_table(tab);
     __syncthreads();
