@@ -1086,7 +1086,9 @@ void launch_l(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEve
             p.stats ? launch_t<L, true, false, true>(sc, p, st, ev)
                     : launch_t<L, true, false, true, false>(sc, p, st, ev);
         else
-            f16 ? launch_t<L, true, false>(sc, p, st, ev) : launch_t<L, false, false>(sc, p, st, ev);
+            f16 ? (p.stats ? launch_t<L, true, false>(sc, p, st, ev)
+                           : launch_t<L, true, false, false, false>(sc, p, st, ev))
+                : launch_t<L, false, false>(sc, p, st, ev);
     }
 }
 

@@ -349,3 +349,18 @@ def test_edge_scenes_match_compiled_reference(ng, torch, case):
     if case["name"] == "empty":
         assert not rgb.any() and not stats[..., 1].any()          # black, no occupied point
         assert np.array_equal(stats[..., 2], stats[..., 0])       # one bit read per point
+
+
+@pytest.mark.parametrize("mlp", ["exact", "tensor"])
+def test_render_without_counters_is_identical(ng, torch, mlp):
+    """Renders that request no per-ray counters run kernel variants with the
+    counter updates compiled out; their RGB must equal the counted render's."""
+    for case in CASES[:3] + [c for c in CASES if c["name"] == "mip360_window"]:
+        scene, cam, opts = make_case(ng, case)
+        dev = ng.Scene(scene)
+        opts.mlp = mlp
+        rgb_s, _ = gpu_render(ng, torch, dev, cam, opts)
+        rgb = ng.render(dev, [cam], opts)
+        torch.cuda.synchronize()
+        rgb = rgb[0].cpu().numpy()
+        assert np.array_equal(rgb.view(np.uint32), rgb_s.view(np.uint32)), case["name"]
