@@ -281,9 +281,13 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
             load_fine_row<F16>(table, (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask,
                                frow[k]);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < 8; ++k) {
+            fine[0] = mac(false, fine[0], w[k], frow[k][0]);
+            fine[1] = mac(FC, fine[1], w[k], frow[k][1]);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) fine[c] = mac(FC && c != 0, fine[c], w[k], frow[k][c]);
+            for (int c = 2; c < 8; c += 2)
+                mac2(FC, fine[c], fine[c + 1], w[k], frow[k][c], frow[k][c + 1]);
+        }
     } else {
 #pragma unroll 1
         for (int k = 0; k < 8; ++k) {
