@@ -114,3 +114,51 @@ def test_bench_two_rank_flow_on_one_gpu():
     d = lines[0]
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"]["value"] > 0
+
+
+def _gpu_tile_worker(rank, world, port, q):
+    """Interleaved 32x32 tiles of one frame rendered by the real kernels on this
+    rank (all ranks share the one GPU of the box), gathered to rank 0 (gloo)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+        import paper_2407_10482_b200 as ng
+        from cases import CASE_BY_NAME, make_case
+        scene, cam, _ = make_case(ng, CASE_BY_NAME["bench_l2"])
+        Wf, Hf = 72, 56   # not a multiple of the 32-pixel tile
+        cam = ng.cameras(4, Wf, Hf)[1]
+        dev = ng.Scene(scene)
+        tiles = []
+        for (x0, y0, w, h) in mg.tile_windows(Wf, Hf, 32, rank, world):
+            rgb = ng.render(dev, [cam], ng.Opts(mlp="exact", window=(x0, y0, w, h)))
+            tiles.append(rgb[0].cpu())
+        img = mg.gather_tiles(tiles, Wf, Hf, 32, world)
+        if rank == 0:
+            full = ng.render(dev, [cam], ng.Opts(mlp="exact"))[0].cpu()
+            q.put(("ok", bool(np.array_equal(img.numpy().view(np.uint32),
+                                              full.numpy().view(np.uint32))), None))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_tile_sharded_frame_is_byte_identical_on_gpu():
+    """SPEC.md:329-330 / SURVEY §8(e): a frame rendered as interleaved tiles by 2
+    ranks and gathered equals the single-render frame bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_tile_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    status, same, _ = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert status == "ok", same
+    assert same
