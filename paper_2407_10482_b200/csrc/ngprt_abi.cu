@@ -74,10 +74,12 @@ struct ngprt_scene {
     };
     mutable HostCtx host;
     // ngprt_render_host_async: two frame slots (device outputs + completion
-    // events), one render stream, one copy stream.
+    // events), each with its own render stream (consecutive frames overlap: the
+    // next frame's march starts in the SM slots the previous one's tail frees),
+    // and one copy stream (frames reach the host in call order).
     struct AsyncCtx {
         std::mutex mu;
-        cudaStream_t render = nullptr, copy = nullptr;
+        cudaStream_t render[2] = {nullptr, nullptr}, copy = nullptr;
         struct Slot {
             float* rgb = nullptr;
             size_t rgb_cap = 0;
@@ -101,7 +103,8 @@ struct ngprt_scene {
         if (host.copy) cudaStreamDestroy(host.copy);
         if (host.rgb) cudaFree(host.rgb);
         if (host.stats) cudaFree(host.stats);
-        if (async.render) cudaStreamSynchronize(async.render);
+        for (cudaStream_t r : async.render)
+            if (r) cudaStreamSynchronize(r);
         if (async.copy) cudaStreamSynchronize(async.copy);
         for (auto& sl : async.slot) {
             if (sl.rgb) cudaFree(sl.rgb);
@@ -109,7 +112,8 @@ struct ngprt_scene {
             if (sl.rendered) cudaEventDestroy(sl.rendered);
             if (sl.copied) cudaEventDestroy(sl.copied);
         }
-        if (async.render) cudaStreamDestroy(async.render);
+        for (cudaStream_t r : async.render)
+            if (r) cudaStreamDestroy(r);
         if (async.copy) cudaStreamDestroy(async.copy);
         for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
@@ -701,15 +705,16 @@ ngprt_status ngprt_render_host_async(const ngprt_scene* s, const ngprt_camera* c
     const size_t n = size_t(W) * H * size_t(n_cams);
     std::lock_guard<std::mutex> lock(s->async.mu);
     auto& ac = s->async;
-    if (!ac.render) {
-        NG_CUDA(cudaStreamCreateWithFlags(&ac.render, cudaStreamNonBlocking));
+    if (!ac.copy) {
+        for (auto& r : ac.render) NG_CUDA(cudaStreamCreateWithFlags(&r, cudaStreamNonBlocking));
         NG_CUDA(cudaStreamCreateWithFlags(&ac.copy, cudaStreamNonBlocking));
         for (auto& sl : ac.slot) {
             NG_CUDA(cudaEventCreateWithFlags(&sl.rendered, cudaEventDisableTiming));
             NG_CUDA(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
         }
     }
-    auto& sl = ac.slot[ac.next];
+    const int k = ac.next;
+    auto& sl = ac.slot[k];
     ac.next ^= 1;
     if (sl.busy) {  // the frame two back still owns this slot's device buffers
         NG_CUDA(cudaEventSynchronize(sl.copied));
@@ -728,9 +733,9 @@ ngprt_status ngprt_render_host_async(const ngprt_scene* s, const ngprt_camera* c
         sl.stats_cap = n;
     }
     const ngprt_status st = render_impl(s, cams, n_cams, o, sl.rgb, stats_host ? sl.stats : nullptr,
-                                        ac.render);
+                                        ac.render[k]);
     if (st != NGPRT_OK) return st;
-    NG_CUDA(cudaEventRecord(sl.rendered, ac.render));
+    NG_CUDA(cudaEventRecord(sl.rendered, ac.render[k]));
     NG_CUDA(cudaStreamWaitEvent(ac.copy, sl.rendered, 0));
     NG_CUDA(cudaMemcpyAsync(rgb_host, sl.rgb, n * 12, cudaMemcpyDeviceToHost, ac.copy));
     if (stats_host)
@@ -745,9 +750,11 @@ ngprt_status ngprt_render_host_wait(const ngprt_scene* s) {
     if (!s) return fail(NGPRT_EINVAL, "ngprt_render_host_wait: null scene");
     std::lock_guard<std::mutex> lock(s->async.mu);
     auto& ac = s->async;
-    if (!ac.render) return NGPRT_OK;
+    if (!ac.copy) return NGPRT_OK;
     NG_CUDA(cudaSetDevice(s->device));
-    const cudaError_t e1 = cudaStreamSynchronize(ac.render);
+    cudaError_t e1 = cudaStreamSynchronize(ac.render[0]);
+    const cudaError_t e1b = cudaStreamSynchronize(ac.render[1]);
+    if (e1 == cudaSuccess) e1 = e1b;
     const cudaError_t e2 = cudaStreamSynchronize(ac.copy);
     for (auto& sl : ac.slot) sl.busy = false;
     if (e1 != cudaSuccess || e2 != cudaSuccess)
