@@ -20,6 +20,8 @@
 // beta sigmoids a fast exp; everything that reaches density, transmittance,
 // early stop or the counters stays exact. Reference citations are relative to
 // /root/reference/proj/include/ngprt/.
+#include <cstdlib>
+
 #include "render.cuh"
 
 namespace ngprt_dev {
@@ -1071,6 +1073,12 @@ void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEve
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // NGPRT_K1_CARVEOUT=<percent>: shared-memory carveout hint for K1 (tuning only;
+        // the driver's default, a 102 KB shared / 154 KB L1 split at 6 CTAs per SM, is
+        // as fast as the 64 KB split, and a smaller L1 is much slower: DESIGN.md §5)
+        if (const char* cv = getenv("NGPRT_K1_CARVEOUT"))
+            cudaFuncSetAttribute(march_kernel<L, F16, MLPF, FC, STATS>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
         grid = sms * ctas_per_sm_t<L, F16, MLPF, FC, STATS>();
     }
     raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
