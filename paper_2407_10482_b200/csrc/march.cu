@@ -128,6 +128,43 @@ __device__ __forceinline__ void stencil_axis(float x, float h, int res, int& bas
     frac = u - float(i);
 }
 
+// L1 allocation policy of the fine-row and probe-code gathers (tuning;
+// 0 default, 1 L1::no_allocate, 2 L1::evict_first, 3 L1::evict_last).
+#ifndef NGPRT_FINE_L1
+#define NGPRT_FINE_L1 0
+#endif
+#ifndef NGPRT_COARSE_L1
+#define NGPRT_COARSE_L1 0
+#endif
+#ifndef NGPRT_PROBE_L1
+#define NGPRT_PROBE_L1 0
+#endif
+#define NGPRT_L1Q_0 ""
+#define NGPRT_L1Q_1 ".L1::no_allocate"
+#define NGPRT_L1Q_2 ".L1::evict_first"
+#define NGPRT_L1Q_3 ".L1::evict_last"
+#define NGPRT_L1Q_(n) NGPRT_L1Q_##n
+#define NGPRT_L1Q(n) NGPRT_L1Q_(n)
+__device__ __forceinline__ uint4 ldg_fine(const uint4* p) {
+#if NGPRT_FINE_L1 == 0
+    return __ldg(p);
+#else
+    uint4 r;
+    asm("ld.global.nc" NGPRT_L1Q(NGPRT_FINE_L1) ".v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+#endif
+}
+__device__ __forceinline__ uint32_t ldg_probe(const uint16_t* p) {
+#if NGPRT_PROBE_L1 == 0
+    return __ldg(p);
+#else
+    unsigned short r;
+    asm("ld.global.nc" NGPRT_L1Q(NGPRT_PROBE_L1) ".u16 %0, [%1];" : "=h"(r) : "l"(p));
+    return r;
+#endif
+}
+
 // One 32 B fp16 coarse row (one sector) in a single 256-bit load (sm_100
 // ld.global.v8.b32 -> LDG.E.256). NGPRT_COARSE_L2_HINT selects the L2 eviction
 // priority: 0 normal, 1 evict_first, 2 evict_last.
@@ -140,7 +177,7 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
 #elif NGPRT_COARSE_L2_HINT == 2
     asm volatile("ld.global.nc.L2::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
 #else
-    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.nc" NGPRT_L1Q(NGPRT_COARSE_L1) ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
 #endif
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
                    "=r"(r[6]), "=r"(r[7])
@@ -177,7 +214,7 @@ template <bool F16>
 __device__ __forceinline__ void load_fine_row(const void* __restrict__ base,
                                               unsigned long long row, float* out) {
     if constexpr (F16) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4*>(base) + row);
+        const uint4 a = ldg_fine(reinterpret_cast<const uint4*>(base) + row);
         const __half2* h = reinterpret_cast<const __half2*>(&a);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -544,7 +581,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         const uint4* table = reinterpret_cast<const uint4*>(sc.fine[l]);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            fraw[l][k] = __ldg(table + ((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask));
+            fraw[l][k] = ldg_fine(table + ((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask));
     }
     // ---- coarse interpolation (baking.hpp:72-78) ----
     float dec[W];
@@ -800,7 +837,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     for (int a = 0; a < 3; ++a) i0[a] = voxel_1d_clamped(xc[a], sc.occ_h0, r0);
     // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
     const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
-    const uint32_t code = __ldg(sc.probe + pidx);
+    const uint32_t code = ldg_probe(sc.probe + pidx);
     const int e = int(code >> 8) & 7;
     // occupancy_probe counters: e + 1 levels read (5 when level 0 decides).
     // Written branch-free so every empty point reaches next_step on one path.
