@@ -817,6 +817,11 @@ __device__ __forceinline__ uint32_t probe_index(uint32_t x, uint32_t y, uint32_t
 #endif
 }
 
+// voxel_exit_step selection form (1: sign-bit bound offset and a two-level
+// compare-and-select of the smallest ratio; 0: the earlier axis-index form)
+#ifndef NGPRT_EXIT_SEL
+#define NGPRT_EXIT_SEL 1
+#endif
 // One marching point (march, occupancy.hpp:310-324): probe (:218-231) via the
 // per-level-1 probe code; occupied -> park for decode; empty -> next_step (:261-276).
 // Returns false when the ray left the clip interval.
@@ -903,7 +908,13 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
                 // 2/r_k = (2/r0) * 2^k: exponent arithmetic on the (normal) power of two
                 const float two_over_res =
                     __int_as_float(__float_as_int(sc.lvl_two_over_res[0]) + (exit_k << 23));
+#if NGPRT_EXIT_SEL
+                // v + [d > 0] from the sign bit; a zero d (either sign) only reaches the
+                // exact path below, which skips that axis, so its bound is never used
+                bound = __fmaf_rn(float(v + 1 - int(__float_as_uint(d) >> 31)), two_over_res, -1.0f);
+#else
                 bound = __fmaf_rn(float(v + (d > 0.0f ? 1 : 0)), two_over_res, -1.0f);
+#endif
             } else {
                 const float lo = -1.0f + (2.0f * float(v)) / float(res);
                 bound = d > 0.0f ? lo + sc.lvl_two_over_res[exit_k] : lo;
@@ -917,6 +928,22 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
             finite = finite && fabsf(q[a]) < 3.0e38f;
         }
         // smallest approximate ratio, its axis, and the second smallest
+#if NGPRT_EXIT_SEL
+        // two compare-and-select levels carry the numerator and direction of the
+        // smaller ratio along (no axis index). Only used when every q is finite, where
+        // the comparisons agree with fminf / fmaxf.
+        const bool p01 = q[0] <= q[1];
+        const float m01 = p01 ? q[0] : q[1], x01 = p01 ? q[1] : q[0];
+        const float n01 = p01 ? num[0] : num[1], d01 = p01 ? s.ray.d[0] : s.ray.d[1];
+        const bool p2 = m01 <= q[2];
+        const float qmin = p2 ? m01 : q[2], q2nd = p2 ? fminf(x01, q[2]) : m01;
+        float t_exit = kBig;
+        const bool tie = !finite || !(q2nd > qmin + (fabsf(qmin) * 1.52587890625e-5f + 1e-30f));
+        if (!tie) {
+            // finite ratios: some d != 0, so the division is the reference's minimum
+            t_exit = (p2 ? n01 : num[2]) / (p2 ? d01 : s.ray.d[2]);
+        } else {
+#else
         const float m01 = fminf(q[0], q[1]), x01 = fmaxf(q[0], q[1]);
         const float qmin = fminf(m01, q[2]), q2nd = fminf(x01, fmaxf(m01, q[2]));
         const int amin = (q[0] <= q[1] && q[0] <= q[2]) ? 0 : (q[1] <= q[2] ? 1 : 2);
@@ -928,7 +955,8 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
                 const float nsel = amin == 0 ? num[0] : (amin == 1 ? num[1] : num[2]);
                 t_exit = nsel / dsel;
             }
-        } else {  // near-tie or non-finite: every axis exactly, as the reference
+        } else {
+#endif  // near-tie or non-finite: every axis exactly, as the reference
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const float d = s.ray.d[a];
