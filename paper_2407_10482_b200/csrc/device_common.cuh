@@ -138,6 +138,7 @@ struct DevScene {
     // occupancy_probe and the distance read of a marching point.
     const uint16_t* probe;
     int dist_is_l1;                                 // dist_res == r1
+    uint32_t consult_mask;                          // bit k: dist grid exists and r_k < dist_res
     float dist_h;                                   // float(dist_res)/2.0f
     float dist_vox;                                 // float(2.0/dist_res) (DistanceGrid::voxel_size)
     float coarse_h;                                 // float(L_C)/2.0f

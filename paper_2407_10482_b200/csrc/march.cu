@@ -864,11 +864,10 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     // voxel_of clamps the index to [0, res-1], so the unclamped point's voxel is
     // the clamped point's: (x+1)*h < 0 <=> x < -1 and (x+1)*h >= res <=> x >= 1.
     const int* iu = i0;
-    // level resolution without a per-lane indexed constant load (divergent
-    // exit levels would serialise it): r_k = r0 >> k for a power-of-two r0
-    const int res = sc.occ_pow2 ? (r0 >> exit_k) : sc.occ_res[exit_k];
+    // res(exit level) < dist_res as a per-scene bit mask over the levels (no
+    // per-lane indexed constant load: divergent exit levels would serialise it)
     uint32_t g = 0;
-    const bool consult = p.use_grid && sc.dist && res < sc.dist_res;
+    const bool consult = p.use_grid && ((sc.consult_mask >> exit_k) & 1u);
     if (consult) {
         if constexpr (STATS) ++s.n_dist;
         if (sc.dist_is_l1) {
@@ -916,7 +915,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
                 bound = __fmaf_rn(float(v + (d > 0.0f ? 1 : 0)), two_over_res, -1.0f);
 #endif
             } else {
-                const float lo = -1.0f + (2.0f * float(v)) / float(res);
+                const float lo = -1.0f + (2.0f * float(v)) / float(sc.occ_res[exit_k]);
                 bound = d > 0.0f ? lo + sc.lvl_two_over_res[exit_k] : lo;
             }
             num[a] = bound - s.ray.o[a];

@@ -375,6 +375,10 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         }
         ds.occ_pow2 = (r0 & (r0 - 1)) == 0;
         ds.dist_is_l1 = ds.dist_res != 0 && ds.dist_res == ds.occ_res[1];
+        // next_step consults the grid iff res(exit level) < dist_res (occupancy.hpp:267)
+        ds.consult_mask = 0;
+        for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k)
+            if (ds.dist && ds.occ_res[k] < ds.dist_res) ds.consult_mask |= 1u << k;
         ds.dist_h = ds.dist_res ? float(ds.dist_res) / 2.0f : 0.f;
         ds.dist_vox = ds.dist_res ? float(2.0 / ds.dist_res) : 0.f;  // DistanceGrid::voxel_size
         ds.coarse_h = float(ds.L_C) / 2.0f;
