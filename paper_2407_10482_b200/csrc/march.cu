@@ -737,6 +737,15 @@ constexpr int kLaneRows = kLaneSmem ? 10 : 0;  // xc[3], cd[3], fs[4]
 // Scratch-column row of lane field j (0..9) after `base` attention rows.
 __device__ __forceinline__ float& lane_row(float* scr, int base, int j) { return scr[(base + j) * kBlock]; }
 
+// voxel_exit_step's finiteness test (1: one per-ray flag for a zero or subnormal
+// direction component, set in start_ray, plus the selected minimum; 0: every
+// approximate ratio tested at every exit step)
+#ifndef NGPRT_EXIT_FLAG
+#define NGPRT_EXIT_FLAG 1
+#endif
+// Lane::out_idx bit 31 is that flag; pixel indices of one launch stay below 2^31
+// (ngprt_render splits larger camera batches).
+constexpr uint32_t kIdxMask = NGPRT_EXIT_FLAG ? 0x7fffffffu : 0xffffffffu;
 // Per-lane ray state.
 struct Lane {
     Ray ray;
@@ -761,14 +770,15 @@ __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s
     }
     r.c = make_float4(valid ? s.ray.d[0] : 0.f, valid ? s.ray.d[1] : 0.f,
                       valid ? s.ray.d[2] : 0.f, valid ? 1.f : 0.f);
-    p.acc[s.out_idx] = r;
+    const uint32_t idx = s.out_idx & kIdxMask;
+    p.acc[idx] = r;
     if (p.stats) {
         ngprt_ray_stats st;
         st.marching = s.n_march;
         st.occupied = s.n_occ;
         st.occ_acc = s.n_occ_acc;
         st.dist_acc = s.n_dist;
-        p.stats[s.out_idx] = st;
+        p.stats[idx] = st;
     }
 }
 
@@ -789,6 +799,13 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
     s.ray.d[0] = b.x; s.ray.d[1] = b.y; s.ray.d[2] = b.z;
     s.t = a.w;
     s.t1 = b.w;
+#if NGPRT_EXIT_FLAG
+    // a zero or subnormal direction component sends every voxel_exit_step of
+    // this ray to the exact all-axes path (flag in the pixel index's top bit)
+    if (!(fabsf(b.x) >= 1.17549435e-38f && fabsf(b.y) >= 1.17549435e-38f &&
+          fabsf(b.z) >= 1.17549435e-38f))
+        s.out_idx |= ~kIdxMask;
+#endif
     if constexpr (kLaneSmem) {
 #pragma unroll
         for (int j = 3; j < 10; ++j) lane_row(scr, lb, j) = 0.f;
@@ -924,7 +941,9 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
             // d == 0: rcp.approx gives inf, so q is inf or NaN and the axis goes to the
             // exact path below, which skips it as the reference does
             q[a] = num[a] * rd;
+#if !NGPRT_EXIT_FLAG
             finite = finite && fabsf(q[a]) < 3.0e38f;
+#endif
         }
         // smallest approximate ratio, its axis, and the second smallest
 #if NGPRT_EXIT_SEL
@@ -936,6 +955,12 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
         const float n01 = p01 ? num[0] : num[1], d01 = p01 ? s.ray.d[0] : s.ray.d[1];
         const bool p2 = m01 <= q[2];
         const float qmin = p2 ? m01 : q[2], q2nd = p2 ? fminf(x01, q[2]) : m01;
+#if NGPRT_EXIT_FLAG
+        // every |d| >= FLT_MIN: each reciprocal is finite and nonzero and no q is NaN;
+        // an overflowed q (|d| near FLT_MIN) is +-inf: -inf is caught here, +inf
+        // only stands for a true ratio beyond FLT_MAX, which is never the minimum
+        finite = !(s.out_idx & ~kIdxMask) && fabsf(qmin) < 3.0e38f;
+#endif
         float t_exit = kBig;
         const bool tie = !finite || !(q2nd > qmin + (fabsf(qmin) * 1.52587890625e-5f + 1e-30f));
         if (!tie) {

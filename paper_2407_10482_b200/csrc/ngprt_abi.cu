@@ -497,8 +497,12 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     if (W == 0 || H == 0) return NGPRT_OK;
     cudaSetDevice(s->device);
     const size_t per_cam = size_t(W) * H;
+    // K0/K1 index the pixels of one launch in 31 bits (K1 keeps a per-ray flag in bit 31)
+    if (per_cam >= (size_t(1) << 31)) return fail(NGPRT_EINVAL, "frame too large (>= 2^31 pixels)");
+    const int cams_per_launch =
+        int(std::min<size_t>(kMaxCamsPerLaunch, ((size_t(1) << 31) - 1) / per_cam));
     RayAcc* acc = nullptr;
-    const int chunk = std::min(n_cams, kMaxCamsPerLaunch);
+    const int chunk = std::min(n_cams, cams_per_launch);
     const size_t acc_bytes = per_cam * chunk * sizeof(RayAcc);
     const size_t ray_bytes = per_cam * chunk * 2 * sizeof(float4);
     NG_CUDA(cudaMallocAsync(&acc, acc_bytes + ray_bytes + 256, st));
@@ -548,8 +552,8 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         prof_lock.lock();
         s->prof_launches = 0;
     }
-    for (int c0 = 0; c0 < n_cams; c0 += kMaxCamsPerLaunch) {
-        const int nc = std::min(kMaxCamsPerLaunch, n_cams - c0);
+    for (int c0 = 0; c0 < n_cams; c0 += cams_per_launch) {
+        const int nc = std::min(cams_per_launch, n_cams - c0);
         p.n_cams = nc;
         for (int i = 0; i < nc; ++i) {
             const ngprt_camera& cam = cams[c0 + i];
