@@ -134,8 +134,10 @@ struct DevScene {
     // Probe code per level-1 voxel (r1^3 u16): bits 8..10 = e, the number of
     // pyramid levels 4..1 whose bit is set before the first clear one (e = 4:
     // all set, level 0 decides); bits 0..7 = the 8 level-0 child bits when
-    // e == 4, else the distance value G (when dist_res == r1). One load answers
-    // occupancy_probe and the distance read of a marching point.
+    // e == 4, else the distance value G (when dist_res == r1); bits 11..13 = the
+    // exit level (e == 4 ? 0 : 4 - e), bit 14 = consult_mask at that level, bit 15
+    // = (e == 4). One load answers occupancy_probe and the distance read of a
+    // marching point.
     const uint16_t* probe;
     int dist_is_l1;                                 // dist_res == r1
     uint32_t consult_mask;                          // bit k: dist grid exists and r_k < dist_res

@@ -860,13 +860,13 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
     const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
     const uint32_t code = ldg_probe(sc.probe + pidx);
-    const int e = int(code >> 8) & 7;
     // occupancy_probe counters: e + 1 levels read (5 when level 0 decides).
     // Written branch-free so every empty point reaches next_step on one path.
-    if constexpr (STATS) s.n_occ_acc += uint32_t(e) + 1u;
-    // level-0 bit from the code's child byte (no second dependent load)
+    if constexpr (STATS) s.n_occ_acc += ((code >> 8) & 7u) + 1u;
+    // level-0 bit from the code's child byte (no second dependent load), gated
+    // by the code's e == 4 flag
     const uint32_t child = uint32_t(i0[0] & 1) | (uint32_t(i0[1] & 1) << 1) | (uint32_t(i0[2] & 1) << 2);
-    if (e == 4 && ((code >> child) & 1u)) {
+    if ((code >> child) & (code >> 15) & 1u) {
         if constexpr (STATS) ++s.n_occ;
         s.pending = true;
 #pragma unroll
@@ -876,7 +876,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
         }
         return true;
     }
-    const int exit_k = e == 4 ? 0 : 4 - e;
+    const int exit_k = int(code >> 11) & 7;  // e == 4 ? 0 : 4 - e
     // next_step (occupancy.hpp:261-276) on the unclamped point ray.at(t). Its
     // voxel_of clamps the index to [0, res-1], so the unclamped point's voxel is
     // the clamped point's: (x+1)*h < 0 <=> x < -1 and (x+1)*h >= res <=> x >= 1.
@@ -884,7 +884,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     // res(exit level) < dist_res as a per-scene bit mask over the levels (no
     // per-lane indexed constant load: divergent exit levels would serialise it)
     uint32_t g = 0;
-    const bool consult = p.use_grid && ((sc.consult_mask >> exit_k) & 1u);
+    const bool consult = p.use_grid && ((code >> 14) & 1u);
     if (consult) {
         if constexpr (STATS) ++s.n_dist;
         if (sc.dist_is_l1) {
@@ -1225,7 +1225,13 @@ __global__ void probe_code_kernel(const DevScene sc, uint16_t* __restrict__ out)
         } else {
             payload = (sc.dist && sc.dist_is_l1) ? sc.dist[i] : 0u;
         }
-        out[probe_index(uint32_t(x), uint32_t(y), uint32_t(z), uint32_t(r1))] = uint16_t((e << 8) | payload);
+        // decoded fields for the marcher: exit level, whether next_step consults
+        // the distance grid at that level, and the e == 4 flag
+        const uint32_t exit_k = e == 4 ? 0u : uint32_t(4 - e);
+        const uint32_t consult = (sc.consult_mask >> exit_k) & 1u;
+        out[probe_index(uint32_t(x), uint32_t(y), uint32_t(z), uint32_t(r1))] =
+            uint16_t((uint32_t(e) << 8) | payload | (exit_k << 11) | (consult << 14) |
+                     (uint32_t(e == 4) << 15));
     }
 }
 
