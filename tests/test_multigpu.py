@@ -44,13 +44,15 @@ def _worker(rank, world, port, q):
             cam = mg.camera_of(rank, world, step, N_CAMS)
             got = mg.gather_frames(fake_render(cam), world)
             if rank == 0:
-                frames.append((step, [g.clone() for g in got]))
+                # numpy (pickled by value): torch tensors would travel as shared-memory
+                # handles that vanish when this process exits before the parent reads them
+                frames.append((step, [g.numpy().copy() for g in got]))
         # interleaved tile sharding of one frame
         wins = mg.tile_windows(W, H, TILE, rank, world)
         tiles = [fake_render(4, w) for w in wins]
         img = mg.gather_tiles(tiles, W, H, TILE, world)
         if rank == 0:
-            q.put(("ok", frames, img))
+            q.put(("ok", frames, img.numpy().copy()))
     except Exception as e:  # pragma: no cover - surfaced by the assert below
         q.put(("err", repr(e), None))
         raise
@@ -74,8 +76,8 @@ def test_sharded_render_gathers_identically(world):
     for step, got in frames:
         for r in range(world):
             want = fake_render(mg.camera_of(r, world, step, N_CAMS))
-            assert torch.equal(got[r], want)
-    assert torch.equal(img, fake_render(4))
+            assert torch.equal(torch.from_numpy(got[r]), want)
+    assert torch.equal(torch.from_numpy(img), fake_render(4))
 
 
 def test_sharding_covers_every_camera_and_tile_once():
