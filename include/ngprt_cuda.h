@@ -149,7 +149,8 @@ ngprt_status ngprt_scene_info_get(const ngprt_scene* scene, ngprt_scene_info* in
 
 /* Render n_cams frames. rgb_dev: n_cams x h x w x 3 f32 (Image::rgb layout per
  * frame, image.hpp:12-22); stats_dev: n_cams x h x w (nullable). Device
- * pointers, asynchronous on `stream` (cudaStream_t, NULL = legacy default). */
+ * pointers, asynchronous on `stream` (cudaStream_t, NULL = legacy default).
+ * A frame (window) of 2^31 pixels or more is NGPRT_EINVAL. */
 ngprt_status ngprt_render(const ngprt_scene* scene, const ngprt_camera* cams, int n_cams,
                           const ngprt_render_opts* opts, float* rgb_dev,
                           ngprt_ray_stats* stats_dev, void* stream);
