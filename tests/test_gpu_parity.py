@@ -221,6 +221,30 @@ def test_full_1080p_frame_matches_oracle(ng, torch):
     assert psnr(t_rgb, want_rgb) >= PSNR_MIN
 
 
+@pytest.mark.parametrize("config,width,height,cam_i", [
+    ("c1_256", 256, 256, 0), ("c2_blob800", 800, 800, 5), ("c5_2160p", 3840, 2160, 0)])
+def test_full_frame_matches_oracle(ng, torch, config, width, height, cam_i):
+    """Configs 1, 2 and 5 at full size (C1 256^2 L=4; C2 800^2 L=2 2^22; C5 3840x2160
+    L=2 2^22, 8.3 M rays): counters and exact-mode RGB bit-exact vs the C
+    restatement on every ray, the tensor-core mode within the north_star tolerance,
+    and a ragged window at the frame's far corner equal to the crop of the frame."""
+    scene = ng.SynthScene(**dict(ng.CONFIGS[config]))
+    cam = ng.cameras(max(cam_i + 1, 1), width, height)[cam_i]
+    dev = ng.Scene(scene)
+    rgb, stats = gpu_render(ng, torch, dev, cam, ng.Opts(mlp="exact"))
+    o = CpuScene(scene.desc_ptr, "oracle")
+    want_rgb, want_stats = o.render(cam, ng.Opts(mlp="exact").to_c())
+    assert np.array_equal(stats, want_stats)
+    assert np.array_equal(rgb.view(np.uint32), want_rgb.view(np.uint32))
+    assert (want_stats[..., 0] > 0).any() and (want_rgb.sum(-1) > 0).any()  # not a blank frame
+    t_rgb, t_stats = gpu_render(ng, torch, dev, cam, ng.Opts(mlp="tensor"))
+    assert np.array_equal(t_stats, want_stats)
+    assert np.abs(t_rgb - want_rgb).max() <= RGB_TOL
+    assert psnr(t_rgb, want_rgb) >= PSNR_MIN
+    win = ng.render(dev, [cam], ng.Opts(mlp="exact", window=(width - 37, height - 19, 37, 19)))
+    assert np.array_equal(win.cpu().numpy()[0].view(np.uint32), rgb[height - 19:, width - 37:].view(np.uint32))
+
+
 def test_multi_camera_batch_and_window_consistency(ng, torch):
     """A 70-camera batch (two launches of <= 64) equals per-camera renders, and a
     window render equals the crop of the full frame."""
