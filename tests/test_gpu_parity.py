@@ -245,6 +245,25 @@ def test_full_frame_matches_oracle(ng, torch, config, width, height, cam_i):
     assert np.array_equal(win.cpu().numpy()[0].view(np.uint32), rgb[height - 19:, width - 37:].view(np.uint32))
 
 
+def test_c4_64_camera_batch_matches_single_renders_and_oracle(ng, torch):
+    """Config 4 at full size: one launch of 64 1080p cameras. Every camera's
+    counters and RGB equal its own single-camera render, and the last camera
+    (largest camera offset in the batch index math) is bit-exact vs the oracle."""
+    scene = ng.SynthScene(**dict(ng.CONFIGS["c4_1080p_x64"]))
+    cams = ng.cameras(64, 1920, 1080)
+    dev = ng.Scene(scene)
+    opts = ng.Opts(mlp="exact")
+    rgb, st = ng.render(dev, cams, opts, stats=True)
+    torch.cuda.synchronize()
+    for i in [0, 17, 42, 63]:
+        one_rgb, one_st = gpu_render(ng, torch, dev, cams[i], opts)
+        assert np.array_equal(st[i].cpu().numpy().view(np.uint32), one_st), i
+        assert np.array_equal(rgb[i].cpu().numpy().view(np.uint32), one_rgb.view(np.uint32)), i
+    want_rgb, want_stats = CpuScene(scene.desc_ptr, "oracle").render(cams[63], opts.to_c())
+    assert np.array_equal(st[63].cpu().numpy().view(np.uint32), want_stats)
+    assert np.array_equal(rgb[63].cpu().numpy().view(np.uint32), want_rgb.view(np.uint32))
+
+
 def test_multi_camera_batch_and_window_consistency(ng, torch):
     """A 70-camera batch (two launches of <= 64) equals per-camera renders, and a
     window render equals the crop of the full frame."""
