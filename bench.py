@@ -189,43 +189,62 @@ def cpu_sample(scene_synth, cam, W, H, seconds, kind_pref="reference"):
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference's CPU render path (oracle/_ref,
+    the reference headers compiled in place; the C restatement when that is
+    absent), on every host thread, one FULL frame of the same config and camera
+    sequence per step (same_config). It loads no product library: the scene and
+    cameras come from the synthetic-scene generator linked into the checker."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import paper_2407_10482_b200 as ng
-    cfg = scene_config(ng, args)
-    W, H = cfg["width"], cfg["height"]
-    scene = ng.SynthScene(**cfg)
-    UNIT = f"fps ({W}x{H} frames/s, all GPUs)"
-    cams = ng.cameras(N_CAMS, W, H)
+    import paper_2407_10482_b200 as ng  # host structs only; the product .so stays unloaded
     sys.path.insert(0, str(ROOT / "tests"))
+    import checkers
     from checkers import REF_SO, CpuScene
     kind = "reference" if REF_SO.exists() else "port"
+    gen = checkers.ref() if kind == "reference" else checkers.oracle_synth()
+    cfg = scene_config(ng, args)
+    W, H = cfg["width"], cfg["height"]
+    scene = ng.SynthScene(_lib=gen, **cfg)
+    UNIT = f"fps ({W}x{H} frames/s, all GPUs)"
+    n_cams = max(N_CAMS, int(cfg.get("n_cams", 1)))
+    cams = ng.cameras(n_cams, W, H, _lib=gen)
     cs = CpuScene(scene.desc_ptr, "ref" if kind == "reference" else "oracle")
     threads = os.cpu_count() or 1
-    rows = 36  # bounded sample per step: a 1920x36 band (~69k rays)
+    # warm-up steps: one 8-row band each (page-in of the scene, OpenMP pool start)
     for s in range(args.warmup):
-        cs.render(cams[s % N_CAMS], ng.Opts(window=(0, H // 2, W, 4)).to_c(), nthreads=threads)
+        cs.render(cams[s % n_cams], ng.Opts(window=(0, H // 2, W, 8)).to_c(), nthreads=threads)
     tot, rays = 0.0, 0
-    for s in range(args.steps):
-        # step s samples the band at height (s + 0.5) / steps of the frame, so the
-        # steps together cover the frame evenly (ray cost varies strongly with row)
-        y0 = int((s + 0.5) / args.steps * (H - rows))
+    stats_sum = None
+    for i in range(args.steps):
+        cam = cams[(args.warmup + i) % n_cams]  # the camera run_ours renders at this step (rank 0)
         t = time.perf_counter()
-        cs.render(cams[s % N_CAMS], ng.Opts(window=(0, y0, W, rows)).to_c(), nthreads=threads)
+        _, st = cs.render(cam, ng.Opts().to_c(), nthreads=threads)
         tot += time.perf_counter() - t
-        rays += W * rows
+        rays += W * H
+        m = st.reshape(-1, 4).astype("float64").mean(0)
+        stats_sum = m if stats_sum is None else stats_sum + m
     fps = rays / tot / (W * H)
+    ms = stats_sum / max(1, args.steps)
     line = {"metric": METRIC, "value": fps, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "mrays_per_s": rays / tot / 1e6,
-            "config": {"workload": f"{args.config}: {W}x{H}, host CPU reference render path",
-                       "step": f"bounded sample: one {W}x{rows} band per step, bands spread "
-                               f"evenly over the frame height across the steps"},
+            "config": {"workload": f"{args.config}: {W}x{H}, host CPU reference render path "
+                                   f"(canonical render_ray composition, SURVEY.md §8(c))",
+                       "step": "one full frame per step, camera (warmup + i) % "
+                               f"{n_cams} of sphere_views({n_cams}, 2.9), as rank 0 of the "
+                               "GPU arm renders",
+                       "same_config": True,
+                       "mean_ray_stats": {"marching": round(float(ms[0]), 2),
+                                          "occupied": round(float(ms[1]), 2),
+                                          "occ_acc": round(float(ms[2]), 2),
+                                          "dist_acc": round(float(ms[3]), 2)},
+                       "libraries": f"{REF_SO.relative_to(ROOT) if kind == 'reference' else 'oracle/_build'}"
+                                    " only (scene generator linked in; no product library)"},
             "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": kind,
-                             "sample": f"{W}x{rows} band per step (step s at height (s+0.5)/steps), "
-                                       f"{threads} OpenMP threads"},
+                             "sample": f"{args.steps} full {W}x{H} frames, {threads} OpenMP threads "
+                                       "(rows scheduled dynamically)"},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line))
@@ -472,10 +491,39 @@ def run_ours(args):
     return 0
 
 
+def launch_ranks(args) -> int:
+    """`--gpus N` without a torch.distributed launcher: re-launch this script as N
+    ranks (torch.distributed.run, one process per GPU, NCCL, rendezvous on
+    127.0.0.1). Fails loudly when fewer than N GPUs are visible, unless
+    NGPRT_BENCH_SHARE_GPU=1 (a functional test of the multi-rank flow on one GPU)."""
+    import socket
+    import torch
+    n_vis = torch.cuda.device_count()
+    if n_vis < args.gpus and not os.environ.get("NGPRT_BENCH_SHARE_GPU"):
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found "
+                         f"{n_vis} (set NGPRT_BENCH_SHARE_GPU=1 to run the ranks on one GPU "
+                         "for a functional test)\n")
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args)  # rank 0 only; other ranks exit at once
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args)
+    _, world, _ = dist_env()
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
     return run_ours(args)
 
 

@@ -199,6 +199,18 @@ ngprt_status ngprt_build_distance_grid(const uint64_t* occ_words_dev, uint32_t r
 ngprt_status ngprt_test_expf(const float* x_dev, float* y_dev, uint64_t n, void* stream);
 ngprt_status ngprt_test_expf_range(uint32_t first_bits, uint64_t n, uint32_t* y_bits_dev,
                                    void* stream);
+/* The K1 marcher (same device code path) over n_rays given rays (8 f32 each:
+ * origin, dir, t_near, t_far; device pointers) with emit(t) always continuing:
+ * records each ray's empty-skip segments (t, t + s) and occupied sample t's, as
+ * the reference's march(..., skip_segments) does (occupancy.hpp:302-326), for the
+ * skip-safety check against dda_oracle. seg: n_rays x max_seg x 2,
+ * samples: n_rays x max_seg, n_seg / n_samples: full counts (may exceed max_seg),
+ * counters: n_rays x 4 (MarchCounters). */
+ngprt_status ngprt_test_march_segments(const ngprt_scene* scene, const float* rays8_dev,
+                                       int n_rays, float step, int use_grid, int max_step_rule,
+                                       int max_seg, float* seg_dev, int* n_seg_dev,
+                                       float* samples_dev, int* n_samples_dev,
+                                       uint32_t* counters_dev, void* stream);
 ngprt_status ngprt_test_hash_index(const int32_t* corners_dev, uint64_t n, uint32_t res,
                                    uint64_t table_len, uint8_t hashed, uint64_t* out_dev,
                                    void* stream);

@@ -180,6 +180,9 @@ SIGNATURES = {
     "ngprt_build_distance_grid": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "ngprt_test_expf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "ngprt_test_expf_range": (C.c_int, [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "ngprt_test_march_segments": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_float, C.c_int,
+                                            C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p]),
     "ngprt_test_hash_index": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint8,
                                         C.c_void_p, C.c_void_p]),
     "ngprt_baked_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
@@ -223,6 +226,20 @@ def lib() -> C.CDLL:
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def bind_synth(L: C.CDLL) -> None:
+    """Set the ngprt_synth_* signatures on a library that exports the synthetic-scene
+    generator (the product library, or oracle/_ref's reference checker, which links
+    the same host-only csrc/synth.cpp)."""
+    if getattr(L, "_ngprt_synth_bound", False):
+        return
+    for name, (res, args) in SIGNATURES.items():
+        if name.startswith("ngprt_synth_") and hasattr(L, name):
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+    L._ngprt_synth_bound = True
 
 
 class NgprtError(RuntimeError):

@@ -1280,6 +1280,65 @@ __global__ void expf_range_kernel(uint32_t first, size_t n, uint32_t* y) {
          i += size_t(gridDim.x) * blockDim.x)
         y[i] = __float_as_uint(glibc_expf(__uint_as_float(first + uint32_t(i)), tab));
 }
+// The marcher K1 runs (march_point, same code path and flags), one thread per
+// given ray, with emit(t) always continuing: records every empty-skip segment
+// (t, t + s) and every occupied sample t, as the reference's march() does with
+// its skip_segments vector (occupancy.hpp:302-326), plus the MarchCounters.
+__global__ void __launch_bounds__(kBlock) march_segments_kernel(
+    const DevScene sc, const MarchParams p, const float* __restrict__ rays8, int n, int max_seg,
+    float* __restrict__ seg, int* __restrict__ nseg, float* __restrict__ samples,
+    int* __restrict__ nsmp, uint32_t* __restrict__ counters) {
+    __shared__ float scratch[kBlock * (kLaneRows > 0 ? kLaneRows : 1)];
+    float* scr = scratch + threadIdx.x;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    Ray r;
+    for (int a = 0; a < 3; ++a) {
+        r.o[a] = rays8[8 * i + a];
+        r.d[a] = rays8[8 * i + 3 + a];
+    }
+    r.tn = rays8[8 * i + 6];
+    r.tf = rays8[8 * i + 7];
+    Lane s;
+    s.ray = r;
+    s.out_idx = 0;
+#if NGPRT_EXIT_FLAG
+    if (!(fabsf(r.d[0]) >= 1.17549435e-38f && fabsf(r.d[1]) >= 1.17549435e-38f &&
+          fabsf(r.d[2]) >= 1.17549435e-38f))
+        s.out_idx |= ~kIdxMask;
+#endif
+    s.n_march = s.n_occ = s.n_occ_acc = s.n_dist = 0;
+    s.pending = false;
+    int ns = 0, nt = 0;
+    float t0, t1;
+    if (clip_f(r, t0, t1)) {  // march(): clip_to_roi<float>, occupancy.hpp:308
+        s.t = t0;
+        s.t1 = t1;
+        while (true) {
+            const float tb = s.t;
+            if (!march_point<true>(sc, p, s, scr, 0)) break;
+            if (s.pending) {
+                if (nt < max_seg) samples[size_t(i) * max_seg + nt] = tb;
+                ++nt;
+                s.pending = false;
+                s.t += p.step;
+            } else {
+                if (ns < max_seg) {
+                    seg[(size_t(i) * max_seg + ns) * 2] = tb;
+                    seg[(size_t(i) * max_seg + ns) * 2 + 1] = s.t;
+                }
+                ++ns;
+            }
+        }
+    }
+    nseg[i] = ns;
+    nsmp[i] = nt;
+    counters[4 * i] = s.n_march;
+    counters[4 * i + 1] = s.n_occ;
+    counters[4 * i + 2] = s.n_occ_acc;
+    counters[4 * i + 3] = s.n_dist;
+}
+
 __global__ void hash_kernel(DevScene sc, const int32_t* c, size_t n, unsigned long long* out) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
          i += size_t(gridDim.x) * blockDim.x)
@@ -1292,6 +1351,16 @@ void launch_test_expf(const float* x, float* y, size_t n, cudaStream_t st) {
 }
 void launch_test_expf_range(uint32_t first, size_t n, uint32_t* y, cudaStream_t st) {
     expf_range_kernel<<<148 * 16, 256, 0, st>>>(first, n, y);
+}
+void launch_test_march_segments(const DevScene& sc, float step, int use_grid, int max_step_rule,
+                                const float* rays8, int n, int max_seg, float* seg, int* nseg,
+                                float* samples, int* nsmp, uint32_t* counters, cudaStream_t st) {
+    MarchParams p{};
+    p.step = step;
+    p.use_grid = use_grid;
+    p.max_step_rule = max_step_rule;
+    march_segments_kernel<<<(n + kBlock - 1) / kBlock, kBlock, 0, st>>>(sc, p, rays8, n, max_seg, seg,
+                                                                      nseg, samples, nsmp, counters);
 }
 void launch_test_hash(const DevScene& sc0, const int32_t* corners, size_t n, int res,
                       unsigned long long len, int mode, uint32_t mask, unsigned long long* out,

@@ -839,6 +839,22 @@ ngprt_status ngprt_test_expf_range(uint32_t first, uint64_t n, uint32_t* y, void
     return NGPRT_OK;
 }
 
+ngprt_status ngprt_test_march_segments(const ngprt_scene* s, const float* rays8, int n_rays,
+                                       float step, int use_grid, int max_step_rule, int max_seg,
+                                       float* seg, int* n_seg, float* samples, int* n_samples,
+                                       uint32_t* counters, void* stream) {
+    if (!s || !rays8 || n_rays < 0 || max_seg < 0 || !seg || !n_seg || !samples || !n_samples ||
+        !counters)
+        return fail(NGPRT_EINVAL, "ngprt_test_march_segments: bad argument");
+    if (n_rays == 0) return NGPRT_OK;
+    NG_CUDA(cudaSetDevice(s->device));
+    launch_test_march_segments(s->ds, step > 0 ? step : float(2.0 * std::sqrt(3.0) / 512.0),
+                               use_grid, max_step_rule, rays8, n_rays, max_seg, seg, n_seg, samples,
+                               n_samples, counters, static_cast<cudaStream_t>(stream));
+    NG_CUDA(cudaGetLastError());
+    return NGPRT_OK;
+}
+
 ngprt_status ngprt_test_hash_index(const int32_t* corners, uint64_t n, uint32_t res,
                                    uint64_t table_len, uint8_t hashed, uint64_t* out,
                                    void* stream) {

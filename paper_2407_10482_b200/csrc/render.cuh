@@ -71,6 +71,9 @@ void launch_convert_fine(const float* src, void* dst, size_t n, int f16, cudaStr
 // test hooks
 void launch_test_expf(const float* x, float* y, size_t n, cudaStream_t st);
 void launch_test_expf_range(uint32_t first, size_t n, uint32_t* y, cudaStream_t st);
+void launch_test_march_segments(const DevScene& sc, float step, int use_grid, int max_step_rule,
+                                const float* rays8, int n, int max_seg, float* seg, int* nseg,
+                                float* samples, int* nsmp, uint32_t* counters, cudaStream_t st);
 void launch_test_hash(const DevScene& sc, const int32_t* corners, size_t n, int res,
                       unsigned long long len, int mode, uint32_t mask,
                       unsigned long long* out, cudaStream_t st);

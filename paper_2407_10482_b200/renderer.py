@@ -39,13 +39,18 @@ CONFIGS = {
     # 2. 800x800 Blender-style bounded blob, 100-camera orbit (EncodingConfig{} defaults)
     "c2_blob800": dict(occupancy="blob", occ_base_res=512, L=2, L_C=512, fine_table_len=1 << 22,
                        width=800, height=800, n_cams=100),
-    # 3. 1920x1080 Mip-NeRF-360-shaped scene, 2^21 entries/level (the 108 fps headline)
-    "c3_1080p": dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
-                     fine_table_len=1 << 21, sigma_lo=1.0, sigma_hi=4.0,
+    # 3. 1920x1080 Mip-NeRF-360-shaped scene, 2^21 entries/level (the 108 fps headline),
+    #    calibrated to PAPER Table 4 (46.7 marching / 17.3 occupied points per ray)
+    "c3_1080p": dict(occupancy="mip360c", n_boxes=16, occ_base_res=512, L=2, L_C=512,
+                     fine_table_len=1 << 21, sigma_lo=1.9, sigma_hi=4.9,
                      width=1920, height=1080, n_cams=1),
-    # 4. 1080p 64-camera batch (sharded across GPUs)
-    "c4_1080p_x64": dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
-                         fine_table_len=1 << 21, sigma_lo=1.0, sigma_hi=4.0,
+    # 3'. the round-1 Mip-NeRF-360-shaped preset (60 marching / 13.5 occupied per ray)
+    "c3_mip360": dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
+                      fine_table_len=1 << 21, sigma_lo=1.0, sigma_hi=4.0,
+                      width=1920, height=1080, n_cams=1),
+    # 4. 1080p 64-camera batch (sharded across GPUs), config 3's scene
+    "c4_1080p_x64": dict(occupancy="mip360c", n_boxes=16, occ_base_res=512, L=2, L_C=512,
+                         fine_table_len=1 << 21, sigma_lo=1.9, sigma_hi=4.9,
                          width=1920, height=1080, n_cams=64),
     # 5. 3840x2160, 2^22 entries/level, occupancy sweep (n_boxes)
     "c5_2160p": dict(occupancy="boxes", n_boxes=140, occ_base_res=512, L=2, L_C=512,
@@ -58,9 +63,14 @@ class SynthScene:
     """Seeded synthetic BakedScene in host memory (ngprt_synth_*): the input both
     the GPU renderer and the CPU oracle consume."""
 
-    def __init__(self, **overrides):
+    def __init__(self, _lib=None, **overrides):
+        # _lib: a library exporting the ngprt_synth_* generator (default: the product
+        # library; bench.py's reference arm passes the CPU reference checker, which
+        # links the same generator, so that arm loads no product code)
+        self._lib = L = _lib if _lib is not None else lib()
+        _abi.bind_synth(L)
         p = SynthParams()
-        lib().ngprt_synth_default_params(C.byref(p))
+        L.ngprt_synth_default_params(C.byref(p))
         for k, v in overrides.items():
             if k not in SCENE_KEYS:
                 continue
@@ -71,11 +81,12 @@ class SynthScene:
             setattr(p, k, v)
         self.params = p
         h = C.c_void_p()
-        st = lib().ngprt_synth_create(C.byref(p), C.byref(h))
+        st = L.ngprt_synth_create(C.byref(p), C.byref(h))
         if st != _abi.OK:
-            raise ValueError("ngprt_synth_create failed (bad parameters)")
+            raise ValueError("ngprt_synth_create failed: " +
+                             L.ngprt_synth_last_error().decode(errors="replace"))
         self._h = h
-        self.desc_ptr = lib().ngprt_synth_desc(h)
+        self.desc_ptr = L.ngprt_synth_desc(h)
         self.desc: SceneDesc = self.desc_ptr.contents
 
     # numpy views over the synth-owned arrays (valid while self is alive)
@@ -118,7 +129,7 @@ class SynthScene:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().ngprt_synth_destroy(self._h)
+            self._lib.ngprt_synth_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -234,10 +245,13 @@ def bake(model, train_words=None, train_res: int | None = None, *, cull_step: fl
     return BakedFile(_handle=h)
 
 
-def cameras(n: int, width: int, height: int, radius: float = 2.9):
+def cameras(n: int, width: int, height: int, radius: float = 2.9, _lib=None):
     """sphere_views(n, radius) with synth_dataset intrinsics (scene.hpp:254-265, 388-395)."""
+    L = _lib if _lib is not None else lib()
+    _abi.bind_synth(L)
     cams = (Camera * n)()
-    check(lib().ngprt_synth_cameras(n, radius, width, height, cams), "ngprt_synth_cameras")
+    if L.ngprt_synth_cameras(n, radius, width, height, cams) != _abi.OK:
+        raise ValueError("ngprt_synth_cameras failed")
     return cams
 
 

@@ -122,6 +122,11 @@ def ref():
     return _ref
 
 
+def oracle_synth() -> C.CDLL:
+    """The C restatement's library; it links the synthetic-scene generator too."""
+    return oracle()
+
+
 def fptr(a: np.ndarray):
     assert a.dtype == np.float32 and a.flags.c_contiguous
     return a.ctypes.data_as(F)

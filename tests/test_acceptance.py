@@ -77,3 +77,104 @@ def test_skip_safety_against_dda_oracle(ng):
                     checked += 1
         rs.close()
     assert checked > 1000
+
+
+def _gpu_segments(ng, torch, dev, rays, step, use_grid, msr, max_seg=512):
+    n = rays.shape[0]
+    d_rays = torch.from_numpy(rays).cuda()
+    seg = torch.zeros((n, max_seg, 2), dtype=torch.float32, device="cuda")
+    smp = torch.zeros((n, max_seg), dtype=torch.float32, device="cuda")
+    nseg = torch.zeros(n, dtype=torch.int32, device="cuda")
+    nsmp = torch.zeros(n, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((n, 4), dtype=torch.int32, device="cuda")
+    ng._abi.check(ng.lib().ngprt_test_march_segments(
+        dev.handle, d_rays.data_ptr(), n, C.c_float(step), use_grid, msr, max_seg, seg.data_ptr(),
+        nseg.data_ptr(), smp.data_ptr(), nsmp.data_ptr(), cnt.data_ptr(), None),
+        "ngprt_test_march_segments")
+    torch.cuda.synchronize()
+    return (seg.cpu().numpy(), nseg.cpu().numpy(), smp.cpu().numpy(), nsmp.cpu().numpy(),
+            cnt.cpu().numpy().view(np.uint32))
+
+
+def _check_segments_against_reference(ng, R, rs, rays, got, use_grid, msr, max_seg=512):
+    """Every GPU empty-skip segment is the reference march()'s own (bit for bit,
+    same order), and no occupied level-0 voxel lies strictly inside it (dda_oracle)."""
+    seg, nseg, smp, nsmp, cnt = got
+    checked = 0
+    for i in range(rays.shape[0]):
+        ray = np.ascontiguousarray(rays[i])
+        c = np.zeros(4, np.uint32)
+        rseg = np.zeros(2 * 4096, np.float32)
+        rts = np.zeros(4096, np.float32)
+        rn, rm = C.c_int(), C.c_int()
+        R.ref_march_segments(rs.h, fptr(ray), C.c_float(ng.K_BASE_STEP), use_grid, msr,
+                             c.ctypes.data_as(C.POINTER(C.c_uint32)), fptr(rseg), 4096, fptr(rts),
+                             4096, C.byref(rn), C.byref(rm))
+        assert np.array_equal(cnt[i], c), (i, cnt[i], c)
+        assert nseg[i] == rn.value and nsmp[i] == rm.value, (i, nseg[i], rn.value)
+        k = min(int(nseg[i]), max_seg)
+        assert np.array_equal(seg[i, :k].reshape(-1).view(np.uint32),
+                              rseg[: 2 * k].view(np.uint32)), i
+        m = min(int(nsmp[i]), max_seg)
+        assert np.array_equal(smp[i, :m].view(np.uint32), rts[:m].view(np.uint32)), i
+        for j in range(k):
+            t0, t1 = float(seg[i, j, 0]), float(seg[i, j, 1])
+            assert R.ref_dda_hits(rs.h, fptr(ray), C.c_float(t0), C.c_float(t1), 1e-5) == 0, \
+                (i, j, t0, t1)
+            checked += 1
+    return checked
+
+
+@pytest.mark.gpu
+def test_gpu_skip_safety_random_grids(ng):
+    """SPEC.md:414 on the GPU marcher itself: K1's march_point (via the
+    ngprt_test_march_segments hook, same device code) over random rays and random
+    occupancy grids records exactly the reference's skip segments and samples,
+    and dda_oracle finds no occupied voxel inside any GPU segment."""
+    import torch
+    R = ref()
+    assert R is not None, "compiled reference (oracle/_ref) required"
+    rng = np.random.RandomState(5)
+    checked = 0
+    for g in range(6):
+        base = ng.SynthScene(occupancy="slab", occ_base_res=64, L=2, L_C=8, fine_table_len=64)
+        words = random_grid_words(ng, 64, [0.002, 0.01, 0.05][g % 3], 200 + g)
+        np.copyto(base.base_words(), words)
+        rs = CpuScene(base.desc_ptr, "ref")
+        dev = ng.Scene(base)
+        o = rng.uniform(-1.6, 1.6, (120, 3))
+        tgt = rng.uniform(-0.9, 0.9, (120, 3))
+        d = (tgt - o) / np.linalg.norm(tgt - o, axis=1, keepdims=True)
+        rays = np.concatenate([o, d, np.zeros((120, 1)), np.full((120, 1), 10.0)], 1).astype(np.float32)
+        rays[:4, 3:6] = [[1, 0, 0], [0, -1, 0], [0, 0, 1], [0.6, 0.8, 0]]  # axis-aligned / zero comps
+        rays[:4, 0:3] = [[-1.5, 0.1, 0.2], [0.3, 1.5, -0.1], [0.05, 0.05, -1.5], [-1.2, -1.4, 0.3]]
+        for use_grid, msr in [(1, 0), (1, 1), (0, 0)]:
+            got = _gpu_segments(ng, torch, dev, rays, ng.K_BASE_STEP, use_grid, msr)
+            checked += _check_segments_against_reference(ng, R, rs, rays, got, use_grid, msr)
+        rs.close()
+    assert checked > 1000
+
+
+@pytest.mark.gpu
+def test_gpu_skip_safety_calibrated_c3_camera_rays(ng):
+    """The same check on the bench scene (config 3, 512^3 pyramid, 256^3 distance
+    grid) for a sample of camera rays of the bench cameras."""
+    import torch
+    R = ref()
+    assert R is not None, "compiled reference (oracle/_ref) required"
+    scene = ng.SynthScene(**dict(ng.CONFIGS["c3_1080p"]))
+    rs = CpuScene(scene.desc_ptr, "ref")
+    dev = ng.Scene(scene)
+    cams = ng.cameras(64, 1920, 1080)
+    rng = np.random.RandomState(9)
+    rays = []
+    for ci in (5, 12, 24):
+        for _ in range(100):
+            ray = np.zeros(8, np.float32)
+            ok = R.ref_generate_ray(C.byref(cams[ci]), float(rng.randint(0, 1920)) + 0.5,
+                                    float(rng.randint(0, 1080)) + 0.5, fptr(ray))
+            if ok:
+                rays.append(ray)
+    rays = np.stack(rays)
+    got = _gpu_segments(ng, torch, dev, rays, ng.K_BASE_STEP, 1, 0)
+    assert _check_segments_against_reference(ng, R, rs, rays, got, 1, 0) > 1000

@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from cases import CASES, make_case, random_grid_words, scene_crc
-from checkers import CpuScene, host_expf_range
+from checkers import REF_SO, CpuScene, host_expf_range
 
 pytestmark = pytest.mark.gpu
 
@@ -199,16 +199,24 @@ def test_expf_exhaustive_vs_host_glibc(ng, torch):
     assert bad == 0
 
 
-def test_full_1080p_frame_matches_oracle(ng, torch):
-    """Config 3 at full size: every ray of a 1920x1080 frame, bit-exact vs the
-    C restatement (counters and RGB)."""
-    cfg = dict(ng.CONFIGS["c3_1080p"])
+def ref_scene(desc_ptr):
+    """The compiled reference (oracle/_ref) holding this scene; required on the GPU box."""
+    assert REF_SO.exists(), "oracle/_ref/libngprt_ref.so missing (built by __graft_entry__.build())"
+    return CpuScene(desc_ptr, "ref")
+
+
+@pytest.mark.parametrize("config,cam_i", [("c3_1080p", 7), ("c3_mip360", 0)])
+def test_full_1080p_frame_matches_reference(ng, torch, config, cam_i):
+    """Config 3 at full size (the calibrated bench scene and the round-1 mip360
+    preset): every ray of a 1920x1080 frame, bit-exact vs the compiled reference
+    (counters and RGB)."""
+    cfg = dict(ng.CONFIGS[config])
     scene = ng.SynthScene(**cfg)
-    cam = ng.cameras(1, 1920, 1080)[0]
+    cam = ng.cameras(64, 1920, 1080)[cam_i]
     opts = ng.Opts(mlp="exact")
     dev = ng.Scene(scene)
     rgb, stats = gpu_render(ng, torch, dev, cam, opts)
-    o = CpuScene(scene.desc_ptr, "oracle")
+    o = ref_scene(scene.desc_ptr)
     want_rgb, want_stats = o.render(cam, opts.to_c())
     assert np.array_equal(stats, want_stats)
     assert np.array_equal(rgb.view(np.uint32), want_rgb.view(np.uint32))
@@ -223,16 +231,16 @@ def test_full_1080p_frame_matches_oracle(ng, torch):
 
 @pytest.mark.parametrize("config,width,height,cam_i", [
     ("c1_256", 256, 256, 0), ("c2_blob800", 800, 800, 5), ("c5_2160p", 3840, 2160, 0)])
-def test_full_frame_matches_oracle(ng, torch, config, width, height, cam_i):
+def test_full_frame_matches_reference(ng, torch, config, width, height, cam_i):
     """Configs 1, 2 and 5 at full size (C1 256^2 L=4; C2 800^2 L=2 2^22; C5 3840x2160
-    L=2 2^22, 8.3 M rays): counters and exact-mode RGB bit-exact vs the C
-    restatement on every ray, the tensor-core mode within the north_star tolerance,
+    L=2 2^22, 8.3 M rays): counters and exact-mode RGB bit-exact vs the compiled
+    reference on every ray, the tensor-core mode within the north_star tolerance,
     and a ragged window at the frame's far corner equal to the crop of the frame."""
     scene = ng.SynthScene(**dict(ng.CONFIGS[config]))
     cam = ng.cameras(max(cam_i + 1, 1), width, height)[cam_i]
     dev = ng.Scene(scene)
     rgb, stats = gpu_render(ng, torch, dev, cam, ng.Opts(mlp="exact"))
-    o = CpuScene(scene.desc_ptr, "oracle")
+    o = ref_scene(scene.desc_ptr)
     want_rgb, want_stats = o.render(cam, ng.Opts(mlp="exact").to_c())
     assert np.array_equal(stats, want_stats)
     assert np.array_equal(rgb.view(np.uint32), want_rgb.view(np.uint32))
@@ -245,10 +253,11 @@ def test_full_frame_matches_oracle(ng, torch, config, width, height, cam_i):
     assert np.array_equal(win.cpu().numpy()[0].view(np.uint32), rgb[height - 19:, width - 37:].view(np.uint32))
 
 
-def test_c4_64_camera_batch_matches_single_renders_and_oracle(ng, torch):
+def test_c4_64_camera_batch_matches_single_renders_and_reference(ng, torch):
     """Config 4 at full size: one launch of 64 1080p cameras. Every camera's
     counters and RGB equal its own single-camera render, and the last camera
-    (largest camera offset in the batch index math) is bit-exact vs the oracle."""
+    (largest camera offset in the batch index math) is bit-exact vs the compiled
+    reference."""
     scene = ng.SynthScene(**dict(ng.CONFIGS["c4_1080p_x64"]))
     cams = ng.cameras(64, 1920, 1080)
     dev = ng.Scene(scene)
@@ -259,7 +268,7 @@ def test_c4_64_camera_batch_matches_single_renders_and_oracle(ng, torch):
         one_rgb, one_st = gpu_render(ng, torch, dev, cams[i], opts)
         assert np.array_equal(st[i].cpu().numpy().view(np.uint32), one_st), i
         assert np.array_equal(rgb[i].cpu().numpy().view(np.uint32), one_rgb.view(np.uint32)), i
-    want_rgb, want_stats = CpuScene(scene.desc_ptr, "oracle").render(cams[63], opts.to_c())
+    want_rgb, want_stats = ref_scene(scene.desc_ptr).render(cams[63], opts.to_c())
     assert np.array_equal(st[63].cpu().numpy().view(np.uint32), want_stats)
     assert np.array_equal(rgb[63].cpu().numpy().view(np.uint32), want_rgb.view(np.uint32))
 
@@ -327,14 +336,14 @@ def test_errors_are_reported(ng, torch):
 
 
 @pytest.mark.parametrize("mlp", ["exact", "tensor"])
-def test_axis_aligned_rays_match_oracle(ng, torch, mlp):
+def test_axis_aligned_rays_match_reference(ng, torch, mlp):
     """Axis-aligned cameras with odd image sizes: the centre row / column rays
     have direction components that are exactly zero, which voxel_exit_step skips
     (occupancy.hpp:244) and the GPU's approximate-argmin path must hand to its
     exact fallback. Counters bit-exact in both modes, RGB bit-exact in exact mode."""
     scene = ng.SynthScene(occupancy="toy", occ_base_res=128, L=2, L_C=64, fine_table_len=1 << 14)
     dev = ng.Scene(scene)
-    o = CpuScene(scene.desc_ptr, "oracle")
+    o = ref_scene(scene.desc_ptr)
     for (o3, rot) in [((0.13, 0.21, -2.6), np.eye(3)),                      # looks down +z
                       ((-2.7, 0.05, 0.11), np.array([[0, 0, 1], [0, 1, 0], [-1, 0, 0]]))]:
         cam = ng._abi.Camera()

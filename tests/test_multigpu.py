@@ -105,9 +105,9 @@ def test_bench_two_rank_flow_on_one_gpu():
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     env = dict(os.environ, NGPRT_BENCH_BACKEND="gloo", NGPRT_BENCH_SHARE_GPU="1")
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
-                        "--master-port", str(_free_port()), str(root / "bench.py"),
+    env.pop("WORLD_SIZE", None)
+    # `bench.py --gpus 2` launches its own 2 ranks (the driver's direct invocation)
+    r = subprocess.run([sys.executable, str(root / "bench.py"),
                         "--gpus", "2", "--config", "c1_256", "--steps", "3", "--warmup", "3"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -116,6 +116,26 @@ def test_bench_two_rank_flow_on_one_gpu():
     d = lines[0]
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_refuses_more_gpus_than_visible():
+    """`bench.py --gpus N` with fewer than N visible GPUs exits non-zero with a
+    message instead of silently timing one GPU."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    import torch
+    root = Path(__file__).resolve().parents[1]
+    n = torch.cuda.device_count() + 1
+    env = dict(os.environ)
+    for k in ("NGPRT_BENCH_SHARE_GPU", "WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", str(n), "--steps", "3",
+                        "--warmup", "3"], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode != 0
+    assert f"needs {n} visible GPUs" in r.stderr
 
 
 def _gpu_tile_worker(rank, world, port, q):
