@@ -445,9 +445,10 @@ struct Staging {
     }
 };
 
+// one staging pair per device (its stream and pinned chunks belong to that device)
 Staging& staging() {
-    static Staging s;
-    return s;
+    static Staging s[kMaxDevices];
+    return s[current_device()];
 }
 
 void d2h(void* dst, const void* src, size_t bytes) {

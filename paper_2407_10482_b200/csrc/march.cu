@@ -1157,10 +1157,9 @@ int ctas_per_sm_t() {
 
 template <int L, bool F16, bool MLPF, bool FC = false, bool STATS = true>
 void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEvent_t between) {
-    static int grid = 0;
-    if (!grid) {
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
+    static PerDeviceInt grid_of;
+    const int grid = grid_of.get([](int dev) {
+        int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         // NGPRT_K1_CARVEOUT=<percent>: shared-memory carveout hint for K1 (tuning only;
         // the driver's default, a 102 KB shared / 154 KB L1 split at 6 CTAs per SM, is
@@ -1168,8 +1167,8 @@ void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEve
         if (const char* cv = getenv("NGPRT_K1_CARVEOUT"))
             cudaFuncSetAttribute(march_kernel<L, F16, MLPF, FC, STATS>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
-        grid = sms * ctas_per_sm_t<L, F16, MLPF, FC, STATS>();
-    }
+        return sms * ctas_per_sm_t<L, F16, MLPF, FC, STATS>();
+    });
     raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
     if (between) cudaEventRecord(between, st);
     const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);

@@ -375,14 +375,13 @@ void shade_consts_from_psi(const float* psi, ShadeConsts* c) {
 void launch_shade_tensor(const DevScene&, const void* psi_tc, const ShadeConsts& consts,
                          const RayAcc* acc, float* rgb, size_t n_rays, cudaStream_t st) {
     if (!n_rays) return;
-    static int grid = 0;
-    if (!grid) {
+    static PerDeviceInt grid_of;
+    const int grid = grid_of.get([](int dev) {
         cudaFuncSetAttribute(shade_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSmemBytes);
         cudaFuncSetAttribute(shade_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              int(cudaSharedmemCarveoutMaxShared));
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const cudaError_t occ_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, shade_tc_kernel, kThreads, kSmemBytes);
@@ -398,11 +397,11 @@ void launch_shade_tensor(const DevScene&, const void* psi_tc, const ShadeConsts&
         const char* ov = std::getenv("NGPRT_K2_CTAS");
         per_sm = ov ? std::atoi(ov) : 3;
         per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
-        grid = sms * per_sm;
         if (std::getenv("NGPRT_VERBOSE"))
-            std::fprintf(stderr, "[ngprt] shade_tc: %d CTAs/SM, grid %d, smem %d B\n", per_sm, grid,
-                         kSmemBytes);
-    }
+            std::fprintf(stderr, "[ngprt] shade_tc: device %d, %d CTAs/SM, grid %d, smem %d B\n", dev,
+                         per_sm, sms * per_sm, kSmemBytes);
+        return sms * per_sm;
+    });
     const size_t tiles = (n_rays + kM - 1) / kM;
     const int blocks = int(tiles < size_t(grid) ? tiles : size_t(grid));
     shade_tc_kernel<<<blocks, kThreads, kSmemBytes, st>>>(

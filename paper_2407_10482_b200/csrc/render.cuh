@@ -1,9 +1,32 @@
 // render.cuh — launch-parameter types shared by the render kernels and the C ABI.
 #pragma once
 
+#include <mutex>
+
 #include "device_common.cuh"
 
 namespace ngprt_dev {
+
+// One-time setup per device. Kernel attributes (dynamic shared memory limits,
+// carveouts) and the SM-count-derived persistent grids are per device, and the
+// ABI renders on any device from any host thread: each value is computed once
+// per device under std::call_once, for the device current at the call.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+struct PerDeviceInt {
+    std::once_flag once[kMaxDevices];
+    int value[kMaxDevices] = {};
+    template <class F>
+    int get(F&& init) {
+        const int d = current_device();
+        std::call_once(once[d], [&] { value[d] = init(d); });
+        return value[d];
+    }
+};
 
 // One camera, pre-flattened: c2w rows (row-major 3x4), intrinsics, image size.
 struct CamParams {

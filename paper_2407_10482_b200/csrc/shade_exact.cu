@@ -117,17 +117,16 @@ __global__ void __launch_bounds__(kShadeBlock)
 void launch_shade_exact(const DevScene& sc, const RayAcc* acc, float* rgb, size_t n_rays,
                         cudaStream_t st) {
     if (!n_rays) return;
-    static int grid = 0;
-    if (!grid) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+    static PerDeviceInt grid_of;
+    const int grid = grid_of.get([](int dev) {
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(shade_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kColsBytes);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shade_exact_kernel, kShadeBlock,
                                                       kColsBytes);
-        grid = sms * (per_sm > 0 ? per_sm : 1);
-    }
+        return sms * (per_sm > 0 ? per_sm : 1);
+    });
     const size_t need = (n_rays + kShadeBlock - 1) / kShadeBlock;
     const unsigned blocks = unsigned(need < size_t(grid) ? need : size_t(grid));
     shade_exact_kernel<<<blocks, kShadeBlock, kColsBytes, st>>>(sc.psi, acc, rgb, n_rays);

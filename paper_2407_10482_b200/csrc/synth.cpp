@@ -163,7 +163,7 @@ std::vector<Box> make_boxes(const std::string& name, uint64_t seed, uint32_t n_b
         // layout idea as "mip360" (central object, ground, background shell near
         // the ROI faces) with fewer, larger blocks: every ray crosses enough
         // material to reach ~17 occupied samples (early stop with sigma_pre ~
-        // U[1.9, 4.9], renderer.py CONFIGS) while the distance grid keeps the empty
+        // U[1.85, 4.85], renderer.py CONFIGS) while the distance grid keeps the empty
         // steps near 29. `n_boxes` = central blocks (16). DESIGN.md §7 explains why
         // these counts need ~13 % voxel occupancy here rather than the paper's ~2 %.
         Rng rng(seed);
@@ -174,7 +174,7 @@ std::vector<Box> make_boxes(const std::string& name, uint64_t seed, uint32_t n_b
             push(c[0] - half[0], c[1] - half[1], c[2] - half[2], c[0] + half[0], c[1] + half[1],
                  c[2] + half[2], rng.uniform(20.0, 80.0));
         }
-        for (int i = 0; i < 10; ++i) {  // ground patches
+        for (int i = 0; i < 60; ++i) {  // ground patches
             double cx = rng.uniform(-0.9, 0.9), cy = rng.uniform(-0.9, 0.9);
             double hx = rng.uniform(0.02, 0.06), hy = rng.uniform(0.02, 0.06);
             double top = rng.uniform(-0.49, -0.44);

@@ -42,7 +42,7 @@ CONFIGS = {
     # 3. 1920x1080 Mip-NeRF-360-shaped scene, 2^21 entries/level (the 108 fps headline),
     #    calibrated to PAPER Table 4 (46.7 marching / 17.3 occupied points per ray)
     "c3_1080p": dict(occupancy="mip360c", n_boxes=16, occ_base_res=512, L=2, L_C=512,
-                     fine_table_len=1 << 21, sigma_lo=1.9, sigma_hi=4.9,
+                     fine_table_len=1 << 21, sigma_lo=1.85, sigma_hi=4.85,
                      width=1920, height=1080, n_cams=1),
     # 3'. the round-1 Mip-NeRF-360-shaped preset (60 marching / 13.5 occupied per ray)
     "c3_mip360": dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
@@ -50,7 +50,7 @@ CONFIGS = {
                       width=1920, height=1080, n_cams=1),
     # 4. 1080p 64-camera batch (sharded across GPUs), config 3's scene
     "c4_1080p_x64": dict(occupancy="mip360c", n_boxes=16, occ_base_res=512, L=2, L_C=512,
-                         fine_table_len=1 << 21, sigma_lo=1.9, sigma_hi=4.9,
+                         fine_table_len=1 << 21, sigma_lo=1.85, sigma_hi=4.85,
                          width=1920, height=1080, n_cams=64),
     # 5. 3840x2160, 2^22 entries/level, occupancy sweep (n_boxes)
     "c5_2160p": dict(occupancy="boxes", n_boxes=140, occ_base_res=512, L=2, L_C=512,
