@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target wall time of the bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", choices=["cameras", "tiles"], default="cameras",
+                    help="cameras: each rank renders whole frames (weak scaling, the default); "
+                         "tiles: every frame split into interleaved tiles over the ranks")
+    ap.add_argument("--tile", type=int, default=32, help="--shard tiles: tile edge in pixels")
     ap.add_argument("--scene", action="append", default=[],
                     help="override a synthetic-scene parameter, e.g. --scene n_boxes=560")
     return ap.parse_args()
@@ -248,6 +252,151 @@ def run_reference(args):
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line))
+    return 0
+
+
+def run_tiles(args):
+    """--shard tiles: single-frame latency mode (BASELINE configs 4 and 5). Every
+    rank renders its interleaved tile x tile tiles of the SAME frame in one
+    K0/K1/K2 launch (ngprt_render_opts.shard_*), the compact shards are gathered
+    to rank 0 over NCCL and de-interleaved there (ngprt_shard_assemble). A step
+    is one frame of the whole job (strong scaling)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2407_10482_b200 as ng
+    from paper_2407_10482_b200 import multigpu as mg
+
+    rank, world, local = dist_env()
+    backend = os.environ.get("NGPRT_BENCH_BACKEND", "nccl")
+    if os.environ.get("NGPRT_BENCH_SHARE_GPU"):
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
+    cfg = scene_config(ng, args)
+    W, H, T = cfg["width"], cfg["height"], args.tile
+    synth = ng.SynthScene(**cfg)
+    scene = ng.Scene(synth, device=local)
+    info = scene.info()
+    n_cams = max(N_CAMS, int(cfg.get("n_cams", 1)))
+    B = max(1, args.batch)
+    cams = ng.cameras(n_cams, W, H)
+    opts = ng.Opts(mlp=args.mlp, profile=True)
+    UNIT = f"fps ({W}x{H} frames/s, all GPUs)"
+    stream = torch.cuda.current_stream(dev)
+    P = ng.shard_pixels(W, H, world, T)
+    gb = torch.empty((world, B, P, 3), dtype=torch.float32, device=dev) if rank == 0 else None
+    sh = torch.empty((B, P, 3), dtype=torch.float32, device=dev) if world > 1 else gb[0]
+    frame = torch.empty((B, H, W, 3), dtype=torch.float32, device=dev) if rank == 0 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def cams_of(step):
+        return [cams[(step * B + j) % n_cams] for j in range(B)]
+
+    def step_fn(step):
+        mg.render_tile_shard(scene, cams_of(step), opts, rank, world, T, out=sh, stream=stream)
+        if world > 1:
+            dist.gather(sh, gather_list=list(gb.unbind(0)) if rank == 0 else None, dst=0)
+        if rank == 0:
+            ng.shard_assemble(gb, world, B, W, H, T, 3, out=frame, stream=stream)
+
+    b_store = 2 if info.storage == 2 else 4
+    alg, stats_mean = {}, {}
+    for s in range(args.warmup + args.steps):
+        for j, c in enumerate(cams_of(s)):
+            idx = (s * B + j) % n_cams
+            if idx not in alg:
+                _, st = ng.render(scene, [c], ng.Opts(mlp=args.mlp), stats=True)
+                st = st.cpu().numpy()
+                alg[idx] = algorithmic_bytes(st, scene.L, b_store, b_store)
+                stats_mean[idx] = st.reshape(-1, 4).mean(0)
+    for s in range(args.warmup):
+        step_fn(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    k0, k1, k2, launches = [], [], [], 0
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            if not args.no_l2_flush:
+                flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            ev[i][0].record(stream)
+            step_fn(args.warmup + i)
+            ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            z, a, b, n = ng.render_timing3(scene)
+            k0.append(z), k1.append(a), k2.append(b)
+            launches += n + (1 if rank == 0 else 0)
+    total_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    frames = args.steps * B
+    fps = frames / (total_ms / 1e3)
+    # e2e: the same steps plus the D2H read of each assembled frame into pinned
+    # host memory on rank 0, by wall clock (max over ranks)
+    host = torch.empty((B, H, W, 3), dtype=torch.float32).pin_memory() if rank == 0 else None
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step_fn(args.warmup + i)
+        if rank == 0:
+            host.copy_(frame, non_blocking=True)
+    torch.cuda.synchronize()
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_fps = frames / float(t.item())
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        k1_avg = sum(k1) / len(k1)
+        bytes_rank = np.mean([sum(alg[(s * B + j) % n_cams] for j in range(B))
+                              for s in range(args.warmup, args.warmup + args.steps)]) / world
+        achieved = bytes_rank / (k1_avg / 1e3) / 1e9
+        ms = np.mean([stats_mean[(s * B + j) % n_cams] for s in range(args.warmup, args.warmup + args.steps)
+                      for j in range(B)], axis=0)
+        line = {
+            "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": fps / PAPER_FPS,
+            "dtype": "f32 (fp16 feature storage, lossless)", "data": "synthetic",
+            "mrays_per_s": fps * W * H / 1e6,
+            "config": {"workload": f"{args.config}: {W}x{H} '{cfg['occupancy']}' synthetic scene, "
+                                   f"L={scene.L}, one frame per step split over {world} rank(s)",
+                       "l2": "flushed (256 MiB write) before every timed step" if not args.no_l2_flush
+                             else "not flushed",
+                       "mean_ray_stats": {k: round(float(v), 2) for k, v in
+                                          zip(["marching", "occupied", "occ_acc", "dist_acc"], ms)},
+                       "parallelism": f"tile sharding: interleaved {T}x{T} tiles, tile t on rank "
+                                      f"t % {world}, one K0/K1/K2 launch per rank per frame, NCCL "
+                                      "gather of the equal-size compact shards to rank 0, then the "
+                                      "ngprt_shard_assemble de-interleave kernel"},
+            "kernel_ms": {"raygen_K0": sum(k0) / len(k0), "march_K1": k1_avg,
+                          "shade_K2": sum(k2) / len(k2)},
+            "roofline": {"bound": "l2", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "kernel": "march_kernel (K1), rank 0",
+                         "peak_source": peak_src,
+                         "note": "algorithmic bytes of the frame / world per rank"},
+            "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": 168 * B,
+                    "d2h_bytes_per_step": B * W * H * 12,
+                    "timer": "wall clock: render + gather + assemble + D2H of the frame into pinned "
+                             "host memory on rank 0, max over ranks"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -524,7 +673,7 @@ def main():
     if world != args.gpus:
         sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
         return 2
-    return run_ours(args)
+    return run_tiles(args) if args.shard == "tiles" else run_ours(args)
 
 
 if __name__ == "__main__":

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define NGPRT_ABI_VERSION 1
+#define NGPRT_ABI_VERSION 2
 #define NGPRT_MAX_FINE_LEVELS 4 /* kMaxFineLevels, fusion.hpp:33 */
 #define NGPRT_PYRAMID_LEVELS 5  /* kPyramidLevels, occupancy.hpp:104 */
 
@@ -47,7 +47,8 @@ typedef enum {
     NGPRT_ECUDA = 2,        /* CUDA runtime failure (message carries cudaGetErrorString) */
     NGPRT_ENOMEM = 3,       /* device allocation failed */
     NGPRT_EUNSUPPORTED = 4, /* valid in the reference, not implemented here (message says what) */
-    NGPRT_ENODEV = 5        /* no CUDA device / not an sm_100 device */
+    NGPRT_ENODEV = 5,       /* no CUDA device / not an sm_100 device */
+    NGPRT_ENCCL = 6         /* NCCL failure in the multi-device calls (message carries ncclGetErrorString) */
 } ngprt_status;
 
 /* FusionTag, fusion.hpp:44-51 (same numeric values as the .ngrt header byte). */
@@ -116,6 +117,19 @@ typedef struct ngprt_render_opts {
     uint8_t profile;       /* record CUDA events around each kernel (ngprt_render_timing)  */
     uint8_t reserved[2];
     uint32_t x0, y0, w, h; /* pixel window; w == 0 || h == 0 => full frame. Output is w x h. */
+    /* Interleaved-tile sharding of the window over `shard_world` renderers
+     * (SURVEY.md §8(e)): the window is cut into shard_tile x shard_tile pixel
+     * tiles, row-major, and tile T belongs to rank T % shard_world. With
+     * shard_world >= 1 one call renders only this rank's tiles (one K0/K1/K2
+     * launch) into a COMPACT output: per camera ngprt_shard_pixels(w, h,
+     * shard_world, shard_tile) pixels, local tile j (global tile rank + j *
+     * shard_world) at j * shard_tile^2, row-major inside the tile; pixels past
+     * the window edge (and a rank's missing last tile) are black. Every rank's
+     * buffer has the same size, so an all-gather / gather needs no padding step;
+     * ngprt_shard_assemble rebuilds the frames. shard_world 0 = unsharded (row-major window); 1 = every tile, in tile-major order. */
+    uint32_t shard_world, shard_rank;
+    uint32_t shard_tile;   /* multiple of 8 (K1's 4x8 ray tiles); 0 => 32 */
+    uint32_t reserved2;
 } ngprt_render_opts;
 
 /* MarchCounters (occupancy.hpp:197-210), per ray. */
@@ -173,6 +187,52 @@ ngprt_status ngprt_render_host_async(const ngprt_scene* scene, const ngprt_camer
                                      ngprt_ray_stats* stats_host);
 /* Blocks until every frame enqueued with ngprt_render_host_async is in host memory. */
 ngprt_status ngprt_render_host_wait(const ngprt_scene* scene);
+
+/* Interleaved-tile sharding (ngprt_render_opts.shard_*): pixels per camera in
+ * every rank's compact output, ceil(n_tiles / world) * tile^2 with n_tiles =
+ * ceil(w / tile) * ceil(h / tile) (tile 0 => 32, world 0 => 1). */
+uint64_t ngprt_shard_pixels(uint32_t w, uint32_t h, uint32_t world, uint32_t tile);
+/* De-interleave gathered shard outputs into frames (device pointers, async):
+ * shards = world consecutive rank buffers, each n_cams x ngprt_shard_pixels(w,
+ * h, world, tile) x `channels` floats (rank-major, as an all-gather / gather to
+ * one device lays them out); frames = n_cams x h x w x channels. channels = 3
+ * for RGB, 4 for ngprt_ray_stats viewed as u32 words. */
+ngprt_status ngprt_shard_assemble(const float* shards_dev, uint32_t world, uint32_t n_cams,
+                                  uint32_t w, uint32_t h, uint32_t tile, uint32_t channels,
+                                  float* frames_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-device rendering in ONE process: a scene replica per
+ * device, one NCCL communicator per device (ncclCommInitAll), one stream per
+ * device. Rays are independent and the scenes read-only, so the only exchange
+ * is the gather of finished pixels to devices[0] (grouped ncclSend/ncclRecv on
+ * the render streams). NCCL is loaded at run time (libnccl.so.2); a missing
+ * library or an NCCL error is NGPRT_ENCCL. When `devices` repeats a device
+ * (several replicas on one GPU: a functional configuration, not a fast one)
+ * the gather uses device-to-device copies instead of NCCL.
+ * ------------------------------------------------------------------------- */
+typedef struct ngprt_multi ngprt_multi;
+ngprt_status ngprt_multi_create(const ngprt_scene_desc* desc, const int* devices, int n_dev,
+                                ngprt_multi** out);
+void ngprt_multi_destroy(ngprt_multi* m);
+/* 1 when the gather runs over NCCL, 0 when over peer copies (repeated devices). */
+int ngprt_multi_uses_nccl(const ngprt_multi* m);
+/* The replica on devices[i] (owned by m), e.g. for ngprt_scene_info_get. */
+const ngprt_scene* ngprt_multi_scene(const ngprt_multi* m, int i);
+/* One frame per camera, each cut into interleaved tile x tile tiles shared by
+ * all devices (one K0/K1/K2 launch per device per call), gathered to
+ * devices[0] and de-interleaved there into rgb_dev0 (n_cams x h x w x 3, a
+ * devices[0] pointer; stats_dev0 likewise n_cams x h x w, nullable). Enqueued
+ * on stream0 (devices[0]); the other devices run on internal streams ordered
+ * after stream0's prior work. opts->shard_* are ignored (set by the call). */
+ngprt_status ngprt_multi_render_tiles(ngprt_multi* m, const ngprt_camera* cams, int n_cams,
+                                      const ngprt_render_opts* opts, uint32_t tile,
+                                      float* rgb_dev0, ngprt_ray_stats* stats_dev0, void* stream0);
+/* Camera sharding: camera c rendered whole by device c % n_dev, gathered to
+ * devices[0] into rgb_dev0 (n_cams x h x w x 3; stats_dev0 nullable). */
+ngprt_status ngprt_multi_render_cameras(ngprt_multi* m, const ngprt_camera* cams, int n_cams,
+                                        const ngprt_render_opts* opts, float* rgb_dev0,
+                                        ngprt_ray_stats* stats_dev0, void* stream0);
 
 /* Per-kernel device time of the most recent ngprt_render on this scene with
  * opts.profile set: CUDA events recorded on the render stream around the march

@@ -14,8 +14,9 @@ LIB_PATH = Path(os.environ.get("NGPRT_LIB") or
 MAX_FINE_LEVELS = 4
 PYRAMID_LEVELS = 5
 
-OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED, ENODEV = range(6)
-STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ECUDA", 3: "ENOMEM", 4: "EUNSUPPORTED", 5: "ENODEV"}
+OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED, ENODEV, ENCCL = range(7)
+STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ECUDA", 3: "ENOMEM", 4: "EUNSUPPORTED", 5: "ENODEV",
+                6: "ENCCL"}
 
 FUSION = {"sum": 0, "shared_att_inv": 1, "separate_att_inv": 2, "shared_att_v": 3,
           "separate_att_v": 4, "mlp": 5}  # fusion_tag_name, fusion.hpp:53-63
@@ -75,6 +76,10 @@ class RenderOpts(C.Structure):
         ("y0", C.c_uint32),
         ("w", C.c_uint32),
         ("h", C.c_uint32),
+        ("shard_world", C.c_uint32),
+        ("shard_rank", C.c_uint32),
+        ("shard_tile", C.c_uint32),
+        ("reserved2", C.c_uint32),
     ]
 
 
@@ -175,6 +180,20 @@ SIGNATURES = {
                                       C.POINTER(C.c_int)]),
     "ngprt_render_timing3": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                        C.POINTER(C.c_float), C.POINTER(C.c_int)]),
+    "ngprt_shard_pixels": (C.c_uint64, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
+    "ngprt_shard_assemble": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "ngprt_multi_create": (C.c_int, [C.POINTER(SceneDesc), C.POINTER(C.c_int), C.c_int,
+                                     C.POINTER(C.c_void_p)]),
+    "ngprt_multi_destroy": (None, [C.c_void_p]),
+    "ngprt_multi_uses_nccl": (C.c_int, [C.c_void_p]),
+    "ngprt_multi_scene": (C.c_void_p, [C.c_void_p, C.c_int]),
+    "ngprt_multi_render_tiles": (C.c_int, [C.c_void_p, C.POINTER(Camera), C.c_int,
+                                           C.POINTER(RenderOpts), C.c_uint32, C.c_void_p,
+                                           C.c_void_p, C.c_void_p]),
+    "ngprt_multi_render_cameras": (C.c_int, [C.c_void_p, C.POINTER(Camera), C.c_int,
+                                             C.POINTER(RenderOpts), C.c_void_p, C.c_void_p,
+                                             C.c_void_p]),
     "ngprt_build_pyramid": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p * (PYRAMID_LEVELS - 1),
                                       C.c_void_p]),
     "ngprt_build_distance_grid": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),

@@ -32,6 +32,7 @@ UNITS = [
     ("occupancy.cu", []),
     ("bake.cu", ["-fmad=false"]),
     ("ngprt_abi.cu", []),
+    ("multi.cu", []),
     ("synth.cpp", []),
     ("ngrt_io.cpp", []),
 ]

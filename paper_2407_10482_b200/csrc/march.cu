@@ -757,6 +757,20 @@ struct Lane {
     bool has_ray, pending;
 };
 
+// Compact sharded index -> (camera, window pixel); false for a padding slot
+// (ngprt_render_opts.shard_*: local tile j is global tile rank + j * world).
+__device__ __forceinline__ bool shard_pixel(const MarchParams& p, uint32_t idx, uint32_t& cam,
+                                            uint32_t& px, uint32_t& py) {
+    const uint32_t t2 = p.shard_tile * p.shard_tile, per_cam = p.shard_local * t2;
+    cam = idx / per_cam;
+    const uint32_t r = idx - cam * per_cam, j = r / t2, l = r - j * t2;
+    const uint32_t T = p.shard_rank + j * p.shard_world;
+    if (T >= p.shard_tiles) return false;
+    px = (T % p.shard_tiles_x) * p.shard_tile + l % p.shard_tile;
+    py = (T / p.shard_tiles_x) * p.shard_tile + l / p.shard_tile;
+    return px < p.w && py < p.h;
+}
+
 __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s, bool valid,
                                              float* scr, int lb) {
     RayAcc r;
@@ -787,11 +801,25 @@ __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s
 __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, uint32_t slot,
                                           Lane& s, float* scr, int lb) {
     const uint32_t cam = tile / p.tiles_per_cam, tt = tile % p.tiles_per_cam;
-    const uint32_t px = (tt % p.tiles_x) * kRayTileW + (slot % kRayTileW),
-                   py = (tt / p.tiles_x) * kRayTileH + (slot / kRayTileW);
     s.has_ray = false;
-    if (px >= p.w || py >= p.h) return;
-    s.out_idx = (cam * p.h + py) * p.w + px;
+    if (p.shard_world) {
+        // sharded: ray tile tt = (local shard tile j, ray tile inside it); K0 has
+        // already finished the padding pixels
+        const uint32_t j = tt / p.shard_rt_per_tile, sub = tt % p.shard_rt_per_tile;
+        const uint32_t lx = (sub % p.shard_rt_x) * kRayTileW + (slot % kRayTileW),
+                       ly = (sub / p.shard_rt_x) * kRayTileH + (slot / kRayTileW);
+        const uint32_t T = p.shard_rank + j * p.shard_world;
+        if (T >= p.shard_tiles) return;
+        const uint32_t px = (T % p.shard_tiles_x) * p.shard_tile + lx,
+                       py = (T / p.shard_tiles_x) * p.shard_tile + ly;
+        if (px >= p.w || py >= p.h) return;
+        s.out_idx = ((cam * p.shard_local + j) * p.shard_tile + ly) * p.shard_tile + lx;
+    } else {
+        const uint32_t px = (tt % p.tiles_x) * kRayTileW + (slot % kRayTileW),
+                       py = (tt / p.tiles_x) * kRayTileH + (slot / kRayTileW);
+        if (px >= p.w || py >= p.h) return;
+        s.out_idx = (cam * p.h + py) * p.w + px;
+    }
     const float4 a = __ldg(p.rays + 2 * size_t(s.out_idx));
     const float4 b = __ldg(p.rays + 2 * size_t(s.out_idx) + 1);
     if (!(b.w >= 0.0f)) return;  // K0 wrote the result (generate_rays/clip_to_roi miss)
@@ -1124,10 +1152,33 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks<L>) march_kernel(const DevS
 // then clip_to_roi<float>, occupancy.hpp:308). Rays that miss are finished here
 // (black, zero counters); the others are queued for K1 as (o, t0), (d, t1).
 __global__ void __launch_bounds__(256) raygen_kernel(const MarchParams p) {
-    const uint32_t px = blockIdx.x * 32 + (threadIdx.x & 31), py = blockIdx.y * 8 + (threadIdx.x >> 5);
-    const int cam = blockIdx.z;
-    if (px >= p.w || py >= p.h) return;
-    const uint32_t idx = (uint32_t(cam) * p.h + py) * p.w + px;
+    uint32_t px, py, idx;
+    int cam;
+    if (p.shard_world) {
+        // compact sharded index space (one thread per slot, padding included:
+        // pixels past the window and a rank's missing last tile come out black)
+        idx = blockIdx.x * 256 + threadIdx.x;
+        if (idx >= uint32_t(p.n_cams) * p.shard_local * p.shard_tile * p.shard_tile) return;
+        uint32_t c;
+        const bool in = shard_pixel(p, idx, c, px, py);
+        cam = int(c);
+        if (!in) {
+            const_cast<float4*>(p.rays)[2 * size_t(idx) + 1] = make_float4(0.f, 0.f, 0.f, -1.0f);
+            RayAcc a;
+            a.a = make_float4(0.f, 0.f, 0.f, 1.0f);
+            a.b = make_float4(0.f, 0.f, 0.f, 0.f);
+            a.c = make_float4(0.f, 0.f, 0.f, 0.f);
+            p.acc[idx] = a;
+            if (p.stats) p.stats[idx] = ngprt_ray_stats{0u, 0u, 0u, 0u};
+            return;
+        }
+    } else {
+        px = blockIdx.x * 32 + (threadIdx.x & 31);
+        py = blockIdx.y * 8 + (threadIdx.x >> 5);
+        cam = blockIdx.z;
+        if (px >= p.w || py >= p.h) return;
+        idx = (uint32_t(cam) * p.h + py) * p.w + px;
+    }
     Ray r;
     const bool valid = generate_ray(p.cams[cam], double(p.x0 + px) + 0.5, double(p.y0 + py) + 0.5, r);
     float t0 = 0.f, t1 = -1.0f;
@@ -1169,7 +1220,12 @@ void launch_t(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEve
                                  cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
         return sms * ctas_per_sm_t<L, F16, MLPF, FC, STATS>();
     });
-    raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
+    if (p.shard_world) {
+        const uint32_t n = uint32_t(p.n_cams) * p.shard_local * p.shard_tile * p.shard_tile;
+        raygen_kernel<<<(n + 255) / 256, 256, 0, st>>>(p);
+    } else {
+        raygen_kernel<<<dim3((p.w + 31) / 32, (p.h + 7) / 8, p.n_cams), 256, 0, st>>>(p);
+    }
     if (between) cudaEventRecord(between, st);
     const uint32_t tiles = p.tiles_per_cam * uint32_t(p.n_cams);
     const uint32_t need = (tiles + 3) / 4;  // 4 warps per CTA

@@ -475,6 +475,39 @@ void set_l2_window(const ngprt_scene* s, cudaStream_t st, cudaStreamAttrValue* s
     cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
 }
 
+// Interleaved-tile sharding geometry of one call (ngprt_render_opts.shard_*).
+struct Shard {
+    uint32_t world = 0, rank = 0, tile = 0, tiles_x = 0, tiles = 0, local = 0;
+    size_t pixels = 0;  // per camera, compact
+};
+
+uint32_t shard_tile_or_default(uint32_t t) { return t ? t : 32u; }
+
+ngprt_status shard_of(const ngprt_render_opts* o, uint32_t W, uint32_t H, Shard* sh) {
+    *sh = Shard{};
+    if (o->shard_world == 0) return NGPRT_OK;  // unsharded
+    const uint32_t tile = shard_tile_or_default(o->shard_tile);
+    if (tile % 8 || tile > 1024)
+        return fail(NGPRT_EINVAL, "shard_tile must be a multiple of 8 and <= 1024");
+    if (o->shard_rank >= o->shard_world) return fail(NGPRT_EINVAL, "shard_rank >= shard_world");
+    sh->world = o->shard_world;
+    sh->rank = o->shard_rank;
+    sh->tile = tile;
+    sh->tiles_x = (W + tile - 1) / tile;
+    sh->tiles = sh->tiles_x * ((H + tile - 1) / tile);
+    sh->local = (sh->tiles + sh->world - 1) / sh->world;
+    sh->pixels = size_t(sh->local) * tile * tile;
+    return NGPRT_OK;
+}
+
+// Output pixels per camera of a call (compact when sharded).
+size_t out_pixels_per_cam(const ngprt_render_opts* o, uint32_t W, uint32_t H) {
+    if (o->shard_world == 0) return size_t(W) * H;
+    const uint64_t t = shard_tile_or_default(o->shard_tile);
+    const uint64_t n = ((W + t - 1) / t) * ((H + t - 1) / t);
+    return size_t((n + o->shard_world - 1) / o->shard_world * t * t);
+}
+
 ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
                          const ngprt_render_opts* o, float* rgb, ngprt_ray_stats* stats,
                          cudaStream_t st) {
@@ -495,8 +528,10 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         if (!(cam.fx != 0.0) || !(cam.fy != 0.0)) return fail(NGPRT_EINVAL, "zero focal length");
     }
     if (W == 0 || H == 0) return NGPRT_OK;
-    cudaSetDevice(s->device);
-    const size_t per_cam = size_t(W) * H;
+    Shard sh;
+    if (const ngprt_status e = shard_of(o, W, H, &sh)) return e;
+    NG_CUDA(cudaSetDevice(s->device));
+    const size_t per_cam = sh.world ? sh.pixels : size_t(W) * H;
     // K0/K1 index the pixels of one launch in 31 bits (K1 keeps a per-ray flag in bit 31)
     if (per_cam >= (size_t(1) << 31)) return fail(NGPRT_EINVAL, "frame too large (>= 2^31 pixels)");
     const int cams_per_launch =
@@ -547,6 +582,17 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     }
     p.tiles_x = (W + kRayTileW - 1) / kRayTileW;
     p.tiles_per_cam = p.tiles_x * ((H + kRayTileH - 1) / kRayTileH);
+    if (sh.world) {
+        p.shard_world = sh.world;
+        p.shard_rank = sh.rank;
+        p.shard_tile = sh.tile;
+        p.shard_tiles_x = sh.tiles_x;
+        p.shard_tiles = sh.tiles;
+        p.shard_local = sh.local;
+        p.shard_rt_x = sh.tile / kRayTileW;
+        p.shard_rt_per_tile = p.shard_rt_x * (sh.tile / kRayTileH);
+        p.tiles_per_cam = sh.local * p.shard_rt_per_tile;
+    }
     std::unique_lock<std::mutex> prof_lock(s->prof_mu, std::defer_lock);
     if (o->profile) {
         prof_lock.lock();
@@ -607,7 +653,7 @@ ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, i
     for (int c = 1; c < n_cams; ++c)
         if (!window && (cams[c].width != W || cams[c].height != H))
             return fail(NGPRT_EINVAL, "all cameras of one call must share width/height");
-    const size_t per_cam = size_t(W) * H, n = per_cam * size_t(n_cams);
+    const size_t per_cam = out_pixels_per_cam(o, W, H), n = per_cam * size_t(n_cams);
     // One call at a time per scene through the cached stream pair and buffers.
     std::lock_guard<std::mutex> lock(s->host.mu);
     auto& hc = s->host;
@@ -662,6 +708,7 @@ ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, i
     }();
     int nb = band_override > 0 ? band_override : 1;
     nb = std::max(1, std::min<int>(nb, int(H)));
+    if (o->shard_world) nb = 1;  // a sharded call's compact output has no row bands
     while (hc.band_done.size() < size_t(n_cams) * nb) {
         cudaEvent_t e;
         NG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -679,7 +726,7 @@ ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, i
             ob.w = W;
             ob.h = r1 - r0;
             const size_t off = size_t(c) * per_cam + size_t(r0) * W;
-            const size_t cnt = size_t(r1 - r0) * W;
+            const size_t cnt = nb == 1 ? per_cam : size_t(r1 - r0) * W;
             status = render_impl(s, cams + c, 1, &ob, hc.rgb + 3 * off,
                                  stats_host ? hc.stats + off : nullptr, hc.render);
             if (status != NGPRT_OK) break;
@@ -710,7 +757,7 @@ ngprt_status ngprt_render_host_async(const ngprt_scene* s, const ngprt_camera* c
     NG_CUDA(cudaSetDevice(s->device));
     const bool window = o->w && o->h;
     const uint32_t W = window ? o->w : cams[0].width, H = window ? o->h : cams[0].height;
-    const size_t n = size_t(W) * H * size_t(n_cams);
+    const size_t n = out_pixels_per_cam(o, W, H) * size_t(n_cams);
     std::lock_guard<std::mutex> lock(s->async.mu);
     auto& ac = s->async;
     if (!ac.copy) {

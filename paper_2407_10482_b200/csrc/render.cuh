@@ -48,6 +48,10 @@ struct MarchParams {
     int n_cams;
     uint32_t x0, y0, w, h;
     uint32_t tiles_x, tiles_per_cam;  // kRayTileW x kRayTileH ray tiles over the window
+    // Interleaved-tile sharding (ngprt_render_opts.shard_*; shard_world == 0: off).
+    // Output/ray index space: per camera shard_local tiles of shard_tile^2 pixels.
+    uint32_t shard_world, shard_rank, shard_tile, shard_tiles_x, shard_tiles, shard_local;
+    uint32_t shard_rt_x, shard_rt_per_tile;  // K1 ray tiles per shard-tile row / per shard tile
     float step;
     int use_grid, max_step_rule, early_stop, keep_level;
     int decode_min, step_burst;  // K1 warp scheduling policy (tunable, see march.cu)

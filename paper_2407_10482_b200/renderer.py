@@ -276,6 +276,11 @@ class Opts:
     mlp: str = "tensor"          # "tensor" (tcgen05, <= 1e-3) | "exact" (bit-exact CUDA cores)
     window: tuple | None = None  # (x0, y0, w, h)
     profile: bool = False        # per-kernel CUDA-event timing (render_timing())
+    # interleaved-tile sharding (ngprt_render_opts.shard_*): world 0 = off; the
+    # output is then the compact (n, shard_pixels, 3) buffer of this rank's tiles
+    shard_world: int = 0
+    shard_rank: int = 0
+    shard_tile: int = 32
 
     def to_c(self) -> RenderOpts:
         o = RenderOpts()
@@ -288,6 +293,7 @@ class Opts:
         o.mlp_mode = _abi.MLP_EXACT if self.mlp == "exact" else _abi.MLP_TENSOR
         if self.window:
             o.x0, o.y0, o.w, o.h = self.window
+        o.shard_world, o.shard_rank, o.shard_tile = self.shard_world, self.shard_rank, self.shard_tile
         return o
 
 
@@ -328,10 +334,35 @@ class Scene:
         self.close()
 
 
-def _out_shape(cams, opts: Opts):
+def _frame_hw(cams, opts: Opts):
     if opts.window:
         return opts.window[3], opts.window[2]
     return int(cams[0].height), int(cams[0].width)
+
+
+def shard_pixels(width: int, height: int, world: int, tile: int = 32) -> int:
+    """Pixels per camera in each rank's compact sharded output (ngprt_shard_pixels)."""
+    return int(lib().ngprt_shard_pixels(width, height, world, tile))
+
+
+def _out_shape(cams, opts: Opts):
+    """Per-camera output shape: (h, w) for a frame / window, (P,) when sharded."""
+    h, w = _frame_hw(cams, opts)
+    if opts.shard_world:
+        return (shard_pixels(w, h, opts.shard_world, opts.shard_tile),)
+    return (h, w)
+
+
+def _check_out(t, shape, dtype, dev, what):
+    """The C ABI writes through raw pointers: reject anything it would overrun."""
+    import torch
+    numel = 1
+    for d in shape:
+        numel *= d
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or t.device != dev or \
+            not t.is_contiguous() or t.numel() < numel:
+        raise ValueError(f"{what} must be a contiguous {dtype} tensor on {dev} with at least "
+                         f"{numel} elements {tuple(shape)}")
 
 
 def render(scene: Scene, cams, opts: Opts | None = None, out=None, stats: bool = False,
@@ -343,12 +374,16 @@ def render(scene: Scene, cams, opts: Opts | None = None, out=None, stats: bool =
     opts = opts or Opts()
     cams = camera_array(cams)
     n = len(cams)
-    h, w = _out_shape(cams, opts)
+    shp = _out_shape(cams, opts)
     dev = torch.device("cuda", scene.device)
     if out is None:
-        out = torch.empty((n, h, w, 3), dtype=torch.float32, device=dev)
-    st = torch.empty((n, h, w, 4), dtype=torch.int32, device=dev) if stats else None
+        out = torch.empty((n, *shp, 3), dtype=torch.float32, device=dev)
+    else:
+        _check_out(out, (n, *shp, 3), torch.float32, dev, "out")
+    st = torch.empty((n, *shp, 4), dtype=torch.int32, device=dev) if stats else None
     s = stream if stream is not None else torch.cuda.current_stream(dev)
+    if s.device != dev:
+        raise ValueError(f"stream is on {s.device}, the scene on {dev}")
     o = opts.to_c()
     check(lib().ngprt_render(scene.handle, cams, n, C.byref(o), out.data_ptr(),
                              st.data_ptr() if st is not None else None, s.cuda_stream),
@@ -378,9 +413,12 @@ def render_host(scene: Scene, cams, opts: Opts | None = None, out=None, stats=No
     opts = opts or Opts()
     cams = camera_array(cams)
     n = len(cams)
-    h, w = _out_shape(cams, opts)
+    shp = _out_shape(cams, opts)
     if out is None:
-        out = np.empty((n, h, w, 3), np.float32)
+        out = np.empty((n, *shp, 3), np.float32)
+    elif out.dtype != np.float32 or not out.flags.c_contiguous or out.size < n * 3 * int(np.prod(shp)):
+        raise ValueError("out must be a C-contiguous float32 array of at least "
+                         f"{(n, *shp, 3)} elements")
     o = opts.to_c()
     check(lib().ngprt_render_host(scene.handle, cams, n, C.byref(o), out.ctypes.data,
                                   stats.ctypes.data if stats is not None else None),
@@ -429,4 +467,23 @@ def build_distance_grid(words, res: int, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream(words.device)
     check(lib().ngprt_build_distance_grid(words.data_ptr(), res, out.data_ptr(), s.cuda_stream),
           "ngprt_build_distance_grid")
+    return out
+
+
+def shard_assemble(shards, world: int, n_cams: int, width: int, height: int, tile: int = 32,
+                   channels: int = 3, out=None, stream=None):
+    """De-interleave gathered compact shard outputs (world x n_cams x P x channels,
+    rank-major as an all-gather lays them out) into (n_cams, h, w, channels) frames
+    on the same device (ngprt_shard_assemble)."""
+    import torch
+    if out is None:
+        out = torch.empty((n_cams, height, width, channels), dtype=shards.dtype, device=shards.device)
+    P = shard_pixels(width, height, world, tile)
+    _check_out(shards, (world, n_cams, P, channels), shards.dtype, shards.device, "shards")
+    _check_out(out, (n_cams, height, width, channels), shards.dtype, shards.device, "out")
+    if shards.element_size() != 4:
+        raise ValueError("shards must have 4-byte elements (f32 RGB or u32 counters)")
+    s = stream if stream is not None else torch.cuda.current_stream(shards.device)
+    check(lib().ngprt_shard_assemble(shards.data_ptr(), world, n_cams, width, height, tile, channels,
+                                     out.data_ptr(), s.cuda_stream), "ngprt_shard_assemble")
     return out

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol(ng):
     missing = [n for n in declared_functions() if not hasattr(L, n)]
     assert not missing, missing
     assert set(declared_functions()) <= set(ng._abi.SIGNATURES)
-    assert L.ngprt_abi_version() == 1
+    assert L.ngprt_abi_version() == 2
 
 
 def test_struct_layout_matches_c(tmp_path, ng):

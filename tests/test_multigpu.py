@@ -152,15 +152,21 @@ def _gpu_tile_worker(rank, world, port, q):
         Wf, Hf = 72, 56   # not a multiple of the 32-pixel tile
         cam = ng.cameras(4, Wf, Hf)[1]
         dev = ng.Scene(scene)
+        # (a) one ngprt_render call per tile window (the host-side tile path)
         tiles = []
         for (x0, y0, w, h) in mg.tile_windows(Wf, Hf, 32, rank, world):
             rgb = ng.render(dev, [cam], ng.Opts(mlp="exact", window=(x0, y0, w, h)))
             tiles.append(rgb[0].cpu())
         img = mg.gather_tiles(tiles, Wf, Hf, 32, world)
+        # (b) this rank's tiles in ONE launch (compact shard), gathered, de-interleaved
+        shard = mg.render_tile_shard(dev, [cam], ng.Opts(mlp="exact"), rank, world, 32)
+        img2 = mg.gather_tile_shards(shard.cpu(), world, Wf, Hf, 32)  # gloo: host tensors
         if rank == 0:
             full = ng.render(dev, [cam], ng.Opts(mlp="exact"))[0].cpu()
-            q.put(("ok", bool(np.array_equal(img.numpy().view(np.uint32),
-                                              full.numpy().view(np.uint32))), None))
+            same = np.array_equal(img.numpy().view(np.uint32), full.numpy().view(np.uint32))
+            same2 = np.array_equal(img2[0].cpu().numpy().view(np.uint32),
+                                   full.numpy().view(np.uint32))
+            q.put(("ok", bool(same and same2), None))
     except Exception as e:  # pragma: no cover
         q.put(("err", repr(e), None))
         raise
@@ -184,3 +190,26 @@ def test_tile_sharded_frame_is_byte_identical_on_gpu():
         assert p.exitcode == 0
     assert status == "ok", same
     assert same
+
+
+@pytest.mark.gpu
+def test_bench_tile_sharding_mode_two_ranks_on_one_gpu():
+    """`bench.py --shard tiles --gpus 2`: one frame per step split into interleaved
+    tiles over 2 ranks (one launch each), gathered and de-interleaved on rank 0.
+    Functional only (gloo, both ranks on one GPU)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, NGPRT_BENCH_BACKEND="gloo", NGPRT_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--shard", "tiles",
+                        "--config", "c1_256", "--steps", "3", "--warmup", "3"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["gpu_launches"] == 3 * 3 + 3  # rank 0: K0/K1/K2 + assemble per step
