@@ -7,9 +7,12 @@
 //     ngprt::gpu::Scene gs(baked);                  // upload once (ngprt_scene_create)
 //     ngprt::Image img = gs.render(dataset, frame); // == render_ray over every pixel
 //     ngprt::BakedScene b = ngprt::gpu::bake(model, train_grid, opts);  // == bake()
+//     ngprt::gpu::MultiScene ms(baked, {0, 1, 2, 3});  // replicas, NCCL gather to GPU 0
+//     ngprt::Image big = ms.render(dataset, frame);     // tiles over 4 GPUs, same Image
 //
 // Requires the reference headers (/root/reference/proj/include) on the include
-// path and links against paper_2407_10482_b200/_lib/libngprt_cuda.so.
+// path and links against paper_2407_10482_b200/_lib/libngprt_cuda.so (and
+// libcudart for MultiScene's device output buffer).
 // Errors surface as std::runtime_error carrying ngprt_last_error(), like the
 // reference's own exceptions.
 #pragma once
@@ -22,6 +25,9 @@
 #include "ngprt/baking.hpp"
 #include "ngprt/config.hpp"
 #include "ngprt/scene.hpp"
+
+#include <cuda_runtime.h>  // MultiScene's devices[0] output buffer
+
 #include "ngprt_cuda.h"
 
 namespace ngprt::gpu {
@@ -42,39 +48,49 @@ inline void check(ngprt_status s, const char* what) {
 // A BakedScene resident on one B200 (immutable).
 class Scene {
 public:
-    explicit Scene(const BakedScene& s, int device = 0) {
-        ngprt_scene_desc d{};
-        const int L = s.cfg.fine_levels;
-        d.L = uint32_t(L);
-        d.L_C = uint32_t(s.cfg.corner_grid_res);
-        // SparseCoarseGrid (baking.hpp:11-50): keys in row order
-        std::vector<uint64_t> keys(s.coarse.index.size());
-        for (const auto& kv : s.coarse.index) keys[kv.second] = kv.first;
-        d.n_coarse = keys.size();
-        d.coarse_keys = keys.data();
-        d.coarse_rows = s.coarse.rows.data();
-        for (int l = 0; l < L; ++l) {
-            d.fine_res[l] = uint32_t(s.fine[l].resolution);
-            d.fine_table_len[l] = s.fine[l].table_len;
-            d.fine_hashed[l] = s.fine[l].addressing == Addressing::Hashed ? 1 : 0;
-            d.fine_tables[l] = s.fine[l].entries.value.data();
-        }
-        for (int k = 0; k < 3; ++k) {
-            d.psi_w[k] = s.psi.weight[k].value.data();
-            d.psi_b[k] = s.psi.bias[k].value.data();
-        }
-        d.fusion_tag = uint8_t(s.tag);
-        d.att_globals = fusion_is_invariant(s.tag) ? s.fusion.global_pre.value.data() : nullptr;
-        if (s.tag == FusionTag::Mlp)
-            for (int k = 0; k < 2; ++k) {
-                d.fusion_mlp_w[k] = s.fusion.mlp.weight[k].value.data();
-                d.fusion_mlp_b[k] = s.fusion.mlp.bias[k].value.data();
+    // The C-ABI view of a reference BakedScene (pointers into `s`, plus the coarse
+    // keys in row order, which SparseCoarseGrid keeps only in its hash map).
+    struct Desc {
+        ngprt_scene_desc desc{};
+        std::vector<uint64_t> keys;
+        explicit Desc(const BakedScene& s) {
+            ngprt_scene_desc& d = desc;
+            const int L = s.cfg.fine_levels;
+            d.L = uint32_t(L);
+            d.L_C = uint32_t(s.cfg.corner_grid_res);
+            // SparseCoarseGrid (baking.hpp:11-50): keys in row order
+            keys.resize(s.coarse.index.size());
+            for (const auto& kv : s.coarse.index) keys[kv.second] = kv.first;
+            d.n_coarse = keys.size();
+            d.coarse_keys = keys.data();
+            d.coarse_rows = s.coarse.rows.data();
+            for (int l = 0; l < L; ++l) {
+                d.fine_res[l] = uint32_t(s.fine[l].resolution);
+                d.fine_table_len[l] = s.fine[l].table_len;
+                d.fine_hashed[l] = s.fine[l].addressing == Addressing::Hashed ? 1 : 0;
+                d.fine_tables[l] = s.fine[l].entries.value.data();
             }
-        d.occ_base_res = uint32_t(s.pyramid.levels[0].res);
-        for (int k = 0; k < kPyramidLevels; ++k) d.pyramid_words[k] = s.pyramid.levels[k].words.data();
-        d.dist_res = uint32_t(s.distance.resolution);
-        d.dist_values = s.distance.values.empty() ? nullptr : s.distance.values.data();
-        check(ngprt_scene_create(&d, device, &h_), "ngprt_scene_create");
+            for (int k = 0; k < 3; ++k) {
+                d.psi_w[k] = s.psi.weight[k].value.data();
+                d.psi_b[k] = s.psi.bias[k].value.data();
+            }
+            d.fusion_tag = uint8_t(s.tag);
+            d.att_globals = fusion_is_invariant(s.tag) ? s.fusion.global_pre.value.data() : nullptr;
+            if (s.tag == FusionTag::Mlp)
+                for (int k = 0; k < 2; ++k) {
+                    d.fusion_mlp_w[k] = s.fusion.mlp.weight[k].value.data();
+                    d.fusion_mlp_b[k] = s.fusion.mlp.bias[k].value.data();
+                }
+            d.occ_base_res = uint32_t(s.pyramid.levels[0].res);
+            for (int k = 0; k < kPyramidLevels; ++k) d.pyramid_words[k] = s.pyramid.levels[k].words.data();
+            d.dist_res = uint32_t(s.distance.resolution);
+            d.dist_values = s.distance.values.empty() ? nullptr : s.distance.values.data();
+        }
+    };
+
+    explicit Scene(const BakedScene& s, int device = 0) {
+        Desc d(s);
+        check(ngprt_scene_create(&d.desc, device, &h_), "ngprt_scene_create");
     }
     ~Scene() { ngprt_scene_destroy(h_); }
     Scene(const Scene&) = delete;
@@ -119,7 +135,6 @@ public:
 
     ngprt_scene* handle() const { return h_; }
 
-private:
     static ngprt_camera camera_of(const PosedDataset& ds, size_t frame) {
         ngprt_camera cam{};
         for (int i = 0; i < 16; ++i) cam.c2w[i] = ds.frames[frame].c2w[i];
@@ -142,7 +157,72 @@ private:
         return ro;
     }
 
+private:
     ngprt_scene* h_ = nullptr;
+};
+
+// A BakedScene replicated on several B200s driven from this one process
+// (ngprt_multi_*): every frame is split into interleaved
+// tile x tile tiles rendered by all devices at once (one launch per device),
+// gathered to devices[0] over NCCL (ncclCommInitAll) and returned as one Image,
+// identical to Scene::render's. render_cameras() gives each device whole frames.
+class MultiScene {
+public:
+    MultiScene(const BakedScene& s, std::vector<int> devices) : devices_(std::move(devices)) {
+        Scene::Desc d(s);
+        check(ngprt_multi_create(&d.desc, devices_.data(), int(devices_.size()), &h_),
+              "ngprt_multi_create");
+    }
+    ~MultiScene() { ngprt_multi_destroy(h_); }
+    MultiScene(const MultiScene&) = delete;
+    MultiScene& operator=(const MultiScene&) = delete;
+    bool uses_nccl() const { return ngprt_multi_uses_nccl(h_) != 0; }
+
+    Image render(const PosedDataset& ds, size_t frame, const RenderOptions& o = {},
+                 uint32_t tile = 32) const {
+        if (frame >= ds.frames.size()) throw std::out_of_range("render: bad frame index");
+        const ngprt_camera cam = Scene::camera_of(ds, frame);
+        const ngprt_render_opts ro = Scene::opts_of(o);
+        return run(&cam, 1, [&](float* rgb) {
+            return ngprt_multi_render_tiles(h_, &cam, 1, &ro, tile, rgb, nullptr, nullptr);
+        })[0];
+    }
+    // Frames `frames` of ds, frame i rendered whole by device i % n (camera sharding).
+    std::vector<Image> render_cameras(const PosedDataset& ds, const std::vector<size_t>& frames,
+                                      const RenderOptions& o = {}) const {
+        std::vector<ngprt_camera> cams;
+        for (size_t f : frames) {
+            if (f >= ds.frames.size()) throw std::out_of_range("render: bad frame index");
+            cams.push_back(Scene::camera_of(ds, f));
+        }
+        const ngprt_render_opts ro = Scene::opts_of(o);
+        return run(cams.data(), int(cams.size()), [&](float* rgb) {
+            return ngprt_multi_render_cameras(h_, cams.data(), int(cams.size()), &ro, rgb, nullptr,
+                                              nullptr);
+        });
+    }
+
+private:
+    // Renders into a devices[0] buffer (legacy stream) and copies the frames out.
+    template <class F>
+    std::vector<Image> run(const ngprt_camera* cams, int n, F&& call) const {
+        const size_t px = size_t(cams[0].width) * cams[0].height;
+        float* d = nullptr;
+        if (cudaSetDevice(devices_[0]) != cudaSuccess || cudaMalloc(&d, px * n * 12) != cudaSuccess)
+            throw std::runtime_error("MultiScene: device allocation failed");
+        std::unique_ptr<float, cudaError_t (*)(void*)> guard(d, cudaFree);
+        check(call(d), "ngprt_multi_render");
+        std::vector<Image> out;
+        for (int i = 0; i < n; ++i) {
+            out.emplace_back(int(cams[0].width), int(cams[0].height));
+            if (cudaMemcpy(out.back().rgb.data(), d + px * 3 * i, px * 12, cudaMemcpyDeviceToHost) !=
+                cudaSuccess)
+                throw std::runtime_error("MultiScene: device-to-host copy failed");
+        }
+        return out;
+    }
+    std::vector<int> devices_;
+    ngprt_multi* h_ = nullptr;
 };
 
 // One-shot convenience: upload, render one frame.

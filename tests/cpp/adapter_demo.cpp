@@ -160,14 +160,39 @@ int main() {
             async_mismatch += max_abs_diff(sync, imgs[f]) != 0.0;
         }
     }
+    // multi-device drop-in (ngprt_multi_*): one device (NCCL communicator from
+    // ncclCommInitAll) and two replicas on device 0 (peer-copy gather); tile and
+    // camera sharding both equal the single-scene render
+    long multi_mismatch = 0;
+    bool multi_nccl = false;
+    {
+        gpu::RenderOptions exact;
+        exact.exact_mlp = true;
+        gpu::MultiScene one(s, {0});
+        multi_nccl = one.uses_nccl();
+        gpu::MultiScene two(s, {0, 0});
+        std::vector<size_t> all;
+        for (size_t f = 0; f < ds.frames.size(); ++f) all.push_back(f);
+        const std::vector<Image> cams_one = one.render_cameras(ds, all, exact);
+        const std::vector<Image> cams_two = two.render_cameras(ds, all, exact);
+        for (size_t f = 0; f < ds.frames.size(); ++f) {
+            const Image want = gs.render(ds, f, exact);
+            multi_mismatch += max_abs_diff(want, one.render(ds, f, exact, 16)) != 0.0;
+            multi_mismatch += max_abs_diff(want, two.render(ds, f, exact, 8)) != 0.0;
+            multi_mismatch += max_abs_diff(want, cams_one[f]) != 0.0;
+            multi_mismatch += max_abs_diff(want, cams_two[f]) != 0.0;
+        }
+    }
     ngprt_scene_info info{};
     ngprt_scene_info_get(gs.handle(), &info);
     size_t bake_corners = 0;
     const bool bake_same = bake_identical(&bake_corners);
     std::printf("{\"frames\": %zu, \"max_abs_exact\": %.9g, \"max_abs_tensor\": %.9g, "
                 "\"psnr_tensor\": %.3f, \"counter_mismatch\": %ld, \"storage\": %d, "
-                "\"bake_identical\": %s, \"bake_corners\": %zu, \"async_mismatch\": %ld}\n",
+                "\"bake_identical\": %s, \"bake_corners\": %zu, \"async_mismatch\": %ld, "
+                "\"multi_mismatch\": %ld, \"multi_nccl\": %s}\n",
                 ds.frames.size(), worst_exact, worst_tc, min_psnr_tc, counter_mismatch,
-                int(info.storage), bake_same ? "true" : "false", bake_corners, async_mismatch);
+                int(info.storage), bake_same ? "true" : "false", bake_corners, async_mismatch,
+                multi_mismatch, multi_nccl ? "true" : "false");
     return 0;
 }

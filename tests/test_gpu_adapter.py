@@ -33,3 +33,7 @@ def test_adapter_renders_reference_baked_scene():
     assert r["bake_corners"] > 0
     # ngprt::gpu::Scene::render_async + wait (ngprt_render_host_async) == render
     assert r["async_mismatch"] == 0
+    # ngprt::gpu::MultiScene (ngprt_multi_*): NCCL on one device, peer copies for two
+    # replicas on one device; tile and camera sharding == Scene::render
+    assert r["multi_nccl"] is True
+    assert r["multi_mismatch"] == 0
