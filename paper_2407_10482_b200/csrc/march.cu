@@ -33,10 +33,11 @@ constexpr unsigned kFull = 0xffffffffu;
 // CTAs per SM the register allocation targets: 6 (80 registers, 24 warps) for
 // L <= 2, 5 (96 registers) for L = 3, 4, whose wider decode would spill at 80.
 // NGPRT_K1_MIN_BLOCKS overrides both.
+// f32 storage (twice the gathered words per sample) takes 5 at every L (96 registers).
 #ifdef NGPRT_K1_MIN_BLOCKS
-template <int L> constexpr int kMinBlocks = NGPRT_K1_MIN_BLOCKS;
+template <int L, bool F16> constexpr int kMinBlocks = NGPRT_K1_MIN_BLOCKS;
 #else
-template <int L> constexpr int kMinBlocks = L <= 2 ? 6 : 5;
+template <int L, bool F16> constexpr int kMinBlocks = (L <= 2 && F16) ? 6 : 5;
 #endif
 
 struct Ray {
@@ -184,6 +185,27 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
                  : "l"(p));
 }
 
+// The N leading words of an f32 coarse row (16 floats, 64 B = two sectors) with
+// the fewest wide loads: 256 bits, then 128 / 64 as needed (N = 8 + 2L).
+template <int N>
+__device__ __forceinline__ void load_coarse_f32_raw(const void* __restrict__ base,
+                                                    unsigned long long row, uint32_t* r) {
+    const uint4* p = reinterpret_cast<const uint4*>(base) + row * 4;
+    uint32_t a[8];
+    ldg256(p, a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = a[i];
+    if constexpr (N > 12) {
+        uint32_t b[8];
+        ldg256(p + 2, b);
+#pragma unroll
+        for (int i = 0; i < N - 8; ++i) r[8 + i] = b[i];
+    } else if constexpr (N > 8) {
+        const uint4 b = __ldg(p + 2);
+        r[8] = b.x; r[9] = b.y; r[10] = b.z; r[11] = b.w;
+    }
+}
+
 // Row loads: N leading elements of a 16-element row, converted to f32 (exact).
 template <int N, bool F16>
 __device__ __forceinline__ void load_coarse_row(const void* __restrict__ base,
@@ -198,15 +220,10 @@ __device__ __forceinline__ void load_coarse_row(const void* __restrict__ base,
             out[2 * i + 1] = f.y;
         }
     } else {
-        const float4* p = reinterpret_cast<const float4*>(base) + row * 4;
+        uint32_t r[16];
+        load_coarse_f32_raw<N>(base, row, r);
 #pragma unroll
-        for (int q = 0; q < (N + 3) / 4; ++q) {
-            const float4 v = __ldg(p + q);
-            out[4 * q] = v.x;
-            if (4 * q + 1 < N) out[4 * q + 1] = v.y;
-            if (4 * q + 2 < N) out[4 * q + 2] = v.z;
-            if (4 * q + 3 < N) out[4 * q + 3] = v.w;
-        }
+        for (int i = 0; i < N; ++i) out[i] = __uint_as_float(r[i]);
     }
 }
 
@@ -223,10 +240,11 @@ __device__ __forceinline__ void load_fine_row(const void* __restrict__ base,
             out[2 * i + 1] = f.y;
         }
     } else {
-        const float4* p = reinterpret_cast<const float4*>(base) + row * 2;
-        const float4 a = __ldg(p), b = __ldg(p + 1);
-        out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
-        out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
+        // an f32 row is 32 B: one sector, one 256-bit load
+        uint32_t r[8];
+        ldg256(reinterpret_cast<const uint4*>(base) + row * 2, r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = __uint_as_float(r[i]);
     }
 }
 
@@ -508,20 +526,28 @@ template <int L> constexpr int kFineAsync = NGPRT_FINE_ASYNC_LEVELS;
 template <int L> constexpr int kFineAsync = L <= 2 ? 0 : 1;
 #endif
 template <int L> constexpr int kFineA = (L - kFineP<L>) < kFineAsync<L> ? (L - kFineP<L>) : kFineAsync<L>;
-template <int L, bool FC>
+// F16 = false: f32 storage (any scene whose values are not fp16-exact, e.g. a
+// real bake or a reference .ngrt): the same arithmetic on f32 rows (a 64 B
+// coarse row in a 256-bit + 128/256-bit load, a 32 B fine row in one 256-bit
+// load); the rows are twice as wide, so the coarse rows take their own round
+// trip (NGPRT_F32_FINE_PREFETCH fine levels ride along, default 0).
+#ifndef NGPRT_F32_FINE_PREFETCH
+#define NGPRT_F32_FINE_PREFETCH 0
+#endif
+template <int L, bool FC, bool F16 = true>
 __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const float x[3],
                                                   int keep_level, const unsigned long long* tab,
                                                   float* scr, uint4* stage, float out[8]) {
     constexpr int W = 8 + 2 * L;
-    constexpr int P = kFineP<L>;
+    constexpr int P = F16 ? kFineP<L> : (NGPRT_F32_FINE_PREFETCH < L ? NGPRT_F32_FINE_PREFETCH : L);
     // fine levels P .. P+A-1 go to shared memory with cp.async (no registers held
     // while in flight), issued together with the coarse and register-held rows
-    constexpr int A = kFineA<L>;
+    constexpr int A = F16 ? kFineA<L> : 0;
 #ifndef NGPRT_COARSE_FULL_ROW
 #define NGPRT_COARSE_FULL_ROW 1
 #endif
     // u32 words of a coarse row actually loaded (W <= 12: 128+64-bit loads, else one 256-bit)
-    constexpr int CW = (W <= 12 && !NGPRT_COARSE_FULL_ROW) ? 6 : 8;
+    constexpr int CW = !F16 ? W : ((W <= 12 && !NGPRT_COARSE_FULL_ROW) ? 6 : 8);
     // ---- issue: coarse rows ----
     int cb[3];
     float cf[3];
@@ -532,9 +558,11 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
     uint32_t craw[8][CW];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const uint4* p = reinterpret_cast<const uint4*>(sc.coarse) +
-                         size_t(key0 + (k & 1) + ((k >> 1) & 1) * r1 + (k >> 2) * r1 * r1) * 2;
-        if constexpr (CW == 8) {
+        const uint32_t key = key0 + (k & 1) + ((k >> 1) & 1) * r1 + (k >> 2) * r1 * r1;
+        const uint4* p = reinterpret_cast<const uint4*>(sc.coarse) + size_t(key) * 2;
+        if constexpr (!F16) {
+            load_coarse_f32_raw<W>(sc.coarse, key, craw[k]);
+        } else if constexpr (CW == 8) {
             uint32_t r[8];
             ldg256(p, r);
 #pragma unroll
@@ -568,7 +596,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
     }
     if constexpr (A > 0) asm volatile("cp.async.commit_group;" ::: "memory");
     // ---- issue: fine levels 0..P-1 ----
-    uint4 fraw[P > 0 ? P : 1][8];
+    uint32_t fraw[P > 0 ? P : 1][8][F16 ? 4 : 8];
     float ff[P > 0 ? P : 1][3];
 #pragma unroll
     for (int l = 0; l < P; ++l) {
@@ -580,8 +608,15 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
         const uint4* table = reinterpret_cast<const uint4*>(sc.fine[l]);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            fraw[l][k] = ldg_fine(table + ((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask));
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t row = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
+            if constexpr (F16) {
+                const uint4 v = ldg_fine(table + row);
+                fraw[l][k][0] = v.x; fraw[l][k][1] = v.y; fraw[l][k][2] = v.z; fraw[l][k][3] = v.w;
+            } else {
+                ldg256(table + size_t(row) * 2, fraw[l][k]);
+            }
+        }
     }
     // ---- coarse interpolation (baking.hpp:72-78) ----
     float dec[W];
@@ -594,7 +629,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         for (int k = 0; k < 8; ++k)
 #pragma unroll
             for (int i = 0; i < W / 2; ++i) {
-                const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&craw[k][i]));
+                const float2 v = F16 ? __half22float2(*reinterpret_cast<const __half2*>(&craw[k][i]))
+                                     : make_float2(__uint_as_float(craw[k][2 * i]),
+                                                   __uint_as_float(craw[k][2 * i + 1]));
                 if (FC && !exact_channel(2 * i) && !exact_channel(2 * i + 1)) {
                     mac2(true, dec[2 * i], dec[2 * i + 1], w[k], v.x, v.y);
                 } else {
@@ -649,10 +686,11 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         for (int c = 0; c < 8; ++c) fine[c] = 0.0f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const __half2* h = reinterpret_cast<const __half2*>(&fraw[l][k]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const float2 v = __half22float2(h[i]);
+                const float2 v = F16 ? __half22float2(*reinterpret_cast<const __half2*>(&fraw[l][k][i]))
+                                     : make_float2(__uint_as_float(fraw[l][k][2 * i]),
+                                                   __uint_as_float(fraw[l][k][2 * i + 1]));
                 if (FC && i != 0) {
                     mac2(true, fine[2 * i], fine[2 * i + 1], w[k], v.x, v.y);
                 } else {
@@ -712,7 +750,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll 1
     for (int l = P + A; l < L; ++l) {
         float fine[8];
-        fine_level<true, FC>(sc, l, x, fine);
+        fine_level<F16, FC>(sc, l, x, fine);
         if (keep_level > 0 && l + 1 != keep_level) {
 #pragma unroll
             for (int c = 1; c < 8; ++c) fine[c] = 0.0f;
@@ -1032,7 +1070,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
 
 // STATS = false (no per-ray counters requested): the counter updates are compiled out.
 template <int L, bool F16, bool MLPF, bool FC, bool STATS>
-__global__ void __launch_bounds__(kBlock, kMinBlocks<L>) march_kernel(const DevScene sc,
+__global__ void __launch_bounds__(kBlock, kMinBlocks<L, F16>) march_kernel(const DevScene sc,
                                                                    const MarchParams p) {
     __shared__ unsigned long long tab[32];
 #ifndef NGPRT_SCRATCH_ROWS
@@ -1096,9 +1134,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks<L>) march_kernel(const DevS
                 float xq[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) xq[a] = kLaneSmem ? lane_row(scr, lb, a) : s.xc[a];
-                if constexpr (F16 && !MLPF) {
+                if constexpr (!MLPF) {
                     if (sc.fast_decode)
-                        decode_point_fast<L, FC>(sc, xq, p.keep_level, tab, scr, stage, f);
+                        decode_point_fast<L, FC, F16>(sc, xq, p.keep_level, tab, scr, stage, f);
                     else
                         decode_point<L, F16, MLPF>(sc, xq, p.keep_level, tab, scr, f);
                 } else {
@@ -1238,13 +1276,19 @@ void launch_l(const DevScene& sc, const MarchParams& p, cudaStream_t st, cudaEve
     if (mlp) {
         f16 ? launch_t<L, true, true>(sc, p, st, ev) : launch_t<L, false, true>(sc, p, st, ev);
     } else {
-        if (f16 && sc.fast_decode && p.fast_color)
-            p.stats ? launch_t<L, true, false, true>(sc, p, st, ev)
-                    : launch_t<L, true, false, true, false>(sc, p, st, ev);
+        // FC (tensor-MLP mode colour FMA) needs the fast decode; STATS = false when
+        // no per-ray counters are requested
+        const bool fc = sc.fast_decode && p.fast_color;
+        if (f16)
+            fc ? (p.stats ? launch_t<L, true, false, true>(sc, p, st, ev)
+                          : launch_t<L, true, false, true, false>(sc, p, st, ev))
+               : (p.stats ? launch_t<L, true, false>(sc, p, st, ev)
+                          : launch_t<L, true, false, false, false>(sc, p, st, ev));
         else
-            f16 ? (p.stats ? launch_t<L, true, false>(sc, p, st, ev)
-                           : launch_t<L, true, false, false, false>(sc, p, st, ev))
-                : launch_t<L, false, false>(sc, p, st, ev);
+            fc ? (p.stats ? launch_t<L, false, false, true>(sc, p, st, ev)
+                          : launch_t<L, false, false, true, false>(sc, p, st, ev))
+               : (p.stats ? launch_t<L, false, false>(sc, p, st, ev)
+                          : launch_t<L, false, false, false, false>(sc, p, st, ev));
     }
 }
 

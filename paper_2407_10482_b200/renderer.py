@@ -44,6 +44,11 @@ CONFIGS = {
     "c3_1080p": dict(occupancy="mip360c", n_boxes=16, occ_base_res=512, L=2, L_C=512,
                      fine_table_len=1 << 21, sigma_lo=1.85, sigma_hi=4.85,
                      width=1920, height=1080, n_cams=1),
+    # 3 with values that are not fp16-representable: f32 storage (the real-scene case:
+    # any bake or reference .ngrt), bit-exact, twice the gathered bytes
+    "c3_1080p_f32": dict(occupancy="mip360c", n_boxes=16, occ_base_res=512, L=2, L_C=512,
+                         fine_table_len=1 << 21, sigma_lo=1.85, sigma_hi=4.85, fp16_exact=0,
+                         width=1920, height=1080, n_cams=1),
     # 3'. the round-1 Mip-NeRF-360-shaped preset (60 marching / 13.5 occupied per ray)
     "c3_mip360": dict(occupancy="mip360", occ_base_res=512, L=2, L_C=512,
                       fine_table_len=1 << 21, sigma_lo=1.0, sigma_hi=4.0,

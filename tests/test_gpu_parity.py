@@ -205,7 +205,7 @@ def ref_scene(desc_ptr):
     return CpuScene(desc_ptr, "ref")
 
 
-@pytest.mark.parametrize("config,cam_i", [("c3_1080p", 7), ("c3_mip360", 0)])
+@pytest.mark.parametrize("config,cam_i", [("c3_1080p", 7), ("c3_1080p_f32", 11), ("c3_mip360", 0)])
 def test_full_1080p_frame_matches_reference(ng, torch, config, cam_i):
     """Config 3 at full size (the calibrated bench scene and the round-1 mip360
     preset): every ray of a 1920x1080 frame, bit-exact vs the compiled reference
@@ -215,6 +215,7 @@ def test_full_1080p_frame_matches_reference(ng, torch, config, cam_i):
     cam = ng.cameras(64, 1920, 1080)[cam_i]
     opts = ng.Opts(mlp="exact")
     dev = ng.Scene(scene)
+    assert dev.info().storage == (1 if config.endswith("_f32") else 2)  # f32 / fp16 rows
     rgb, stats = gpu_render(ng, torch, dev, cam, opts)
     o = ref_scene(scene.desc_ptr)
     want_rgb, want_stats = o.render(cam, opts.to_c())
