@@ -33,11 +33,13 @@ constexpr unsigned kFull = 0xffffffffu;
 // CTAs per SM the register allocation targets: 6 (80 registers, 24 warps) for
 // L <= 2, 5 (96 registers) for L = 3, 4, whose wider decode would spill at 80.
 // NGPRT_K1_MIN_BLOCKS overrides both.
-// f32 storage (twice the gathered words per sample) takes 5 at every L (96 registers).
+// f32 storage (twice the gathered words per sample, fine level 0 gathered with the
+// coarse rows) takes 4 (128 registers): 4.89 -> 4.76 ms at config 3 vs 5 CTAs
+// without the fine prefetch.
 #ifdef NGPRT_K1_MIN_BLOCKS
 template <int L, bool F16> constexpr int kMinBlocks = NGPRT_K1_MIN_BLOCKS;
 #else
-template <int L, bool F16> constexpr int kMinBlocks = (L <= 2 && F16) ? 6 : 5;
+template <int L, bool F16> constexpr int kMinBlocks = F16 ? (L <= 2 ? 6 : 5) : 4;
 #endif
 
 struct Ray {
@@ -248,6 +250,42 @@ __device__ __forceinline__ void load_fine_row(const void* __restrict__ base,
     }
 }
 
+// The 8 fp16 corner rows of a power-of-two hashed fine level with x-adjacent
+// pairs fetched together (NGPRT_FINE_PAIR). The x prime is 1 (hash_grid.hpp:8):
+// for an even base x the corners x and x + 1 of one (y, z) hash to rows h and
+// h ^ 1, the two halves of one 32 B sector, so one 256-bit load brings both
+// (and the pair swaps when h is odd); an odd base x takes two 128-bit loads.
+// Rows come out in corner order k, so the interpolation is unchanged.
+// NGPRT_FINE_PAIR bit 0: the fine levels gathered with the coarse rows; bit 1:
+// the levels gathered in their own round trip (fine_level).
+#ifndef NGPRT_FINE_PAIR
+#define NGPRT_FINE_PAIR 0
+#endif
+__device__ __forceinline__ void fine_rows_paired(const uint4* __restrict__ table, int bx,
+                                                 const uint32_t hy[2], const uint32_t hz[2],
+                                                 uint32_t mask, uint32_t (&rows)[8][4]) {
+    const bool even = (bx & 1) == 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t c = hy[j & 1] ^ hz[j >> 1];
+        const uint32_t h0 = (uint32_t(bx) ^ c) & mask, h1 = (uint32_t(bx + 1) ^ c) & mask;
+        uint32_t r[8];
+        if (even) {
+            ldg256(table + (h0 & ~1u), r);
+        } else {
+            const uint4 a = ldg_fine(table + h0), b = ldg_fine(table + h1);
+            r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+            r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+        }
+        const bool swap = even && (h0 & 1u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            rows[2 * j][i] = swap ? r[4 + i] : r[i];
+            rows[2 * j + 1][i] = swap ? r[i] : r[4 + i];
+        }
+    }
+}
+
 // HashLevel::hash_index, hash_grid.hpp:83-94 (primes :8-10)
 __device__ __forceinline__ unsigned long long fine_index(const DevScene& sc, int l, int x, int y,
                                                          int z) {
@@ -333,6 +371,20 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
         const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
         const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
         float frow[8][8];
+#if NGPRT_FINE_PAIR & 2
+        if constexpr (F16) {
+            uint32_t raw[8][4];
+            fine_rows_paired(reinterpret_cast<const uint4*>(table), b[0], hy, hz, mask, raw);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&raw[k][i]));
+                    frow[k][2 * i] = f2.x;
+                    frow[k][2 * i + 1] = f2.y;
+                }
+        } else
+#endif
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             load_fine_row<F16>(table, (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask,
@@ -530,9 +582,9 @@ template <int L> constexpr int kFineA = (L - kFineP<L>) < kFineAsync<L> ? (L - k
 // real bake or a reference .ngrt): the same arithmetic on f32 rows (a 64 B
 // coarse row in a 256-bit + 128/256-bit load, a 32 B fine row in one 256-bit
 // load); the rows are twice as wide, so the coarse rows take their own round
-// trip (NGPRT_F32_FINE_PREFETCH fine levels ride along, default 0).
+// trip, and NGPRT_F32_FINE_PREFETCH fine levels ride along (default 1).
 #ifndef NGPRT_F32_FINE_PREFETCH
-#define NGPRT_F32_FINE_PREFETCH 0
+#define NGPRT_F32_FINE_PREFETCH 1
 #endif
 template <int L, bool FC, bool F16 = true>
 __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const float x[3],
@@ -607,6 +659,12 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
         const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
         const uint4* table = reinterpret_cast<const uint4*>(sc.fine[l]);
+#if NGPRT_FINE_PAIR & 1
+        if constexpr (F16) {
+            fine_rows_paired(table, b[0], hy, hz, mask, fraw[l]);
+            continue;
+        }
+#endif
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const uint32_t row = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
