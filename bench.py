@@ -36,6 +36,9 @@ METRIC = "1080p fps & Mrays/s at 1/2/4/8 B200 vs host-CPU ref; achieved L2/HBM G
 UNIT = "fps (1920x1080 frames/s, all GPUs)"
 N_CAMS = 64
 PAPER_FPS = 108.0  # 1080p, L=2, RTX 3090
+L2_NOTE = ("flushed (256 MiB write) before every timed step; the fine hash tables (64 MB at "
+           "2^21 x 2 levels) stay L2-resident through the renderer's access-policy window "
+           "(persisting lines survive the flush by design, north_star)")
 
 
 def parse():
@@ -98,6 +101,22 @@ def algorithmic_bytes(stats, L, b_c=2, b_f=2):
     s = stats.reshape(-1, 4).astype(np.float64)
     per_sample = 8 * ((8 + 2 * L) * b_c + 8 * L * b_f)
     return float((s[:, 1] * per_sample + 4 * s[:, 2] + 1 * s[:, 3]).sum() + 12 * s.shape[0])
+
+
+def binding_ceiling(l2_bytes, dram_bytes, k1_ms, ceilings):
+    """Name the resource that binds K1: its measured L2 sector traffic against the
+    L2-resident random 32 B-gather peak measured on this B200 (the access pattern
+    K1 has), and its DRAM traffic against the HBM copy peak."""
+    if not l2_bytes or not ceilings or "l2_gather32_gbs" not in ceilings:
+        return None
+    l2 = l2_bytes / (k1_ms / 1e3) / 1e9
+    g = ceilings["l2_gather32_gbs"]["peak_gbs"]
+    out = {"ceiling": "L2 random 32 B-sector gather (L2-resident tables)", "peak_gbs": g,
+           "achieved_gbs": l2, "frac": l2 / g}
+    if dram_bytes:
+        peak, _ = load_peaks()
+        out["dram_frac_of_hbm_peak"] = dram_bytes / (k1_ms / 1e3) / 1e9 / peak
+    return out
 
 
 class Clocks:
@@ -373,7 +392,7 @@ def run_tiles(args):
             "mrays_per_s": fps * W * H / 1e6,
             "config": {"workload": f"{args.config}: {W}x{H} '{cfg['occupancy']}' synthetic scene, "
                                    f"L={scene.L}, one frame per step split over {world} rank(s)",
-                       "l2": "flushed (256 MiB write) before every timed step" if not args.no_l2_flush
+                       "l2": L2_NOTE if not args.no_l2_flush
                              else "not flushed",
                        "mean_ray_stats": {k: round(float(v), 2) for k, v in
                                           zip(["marching", "occupied", "occ_acc", "dist_acc"], ms)},
@@ -584,7 +603,7 @@ def run_ours(args):
                        "cameras": f"sphere_views({n_cams}, 2.9); rank r renders cameras "
                                   f"(r + N*(step*{B} + j)) % {n_cams}, j < {B} per step"
                                   + (f" (one ngprt_render call of {B} cameras)" if B > 1 else ""),
-                       "l2": "flushed (256 MiB write) before every timed step" if not args.no_l2_flush
+                       "l2": L2_NOTE if not args.no_l2_flush
                              else "not flushed; scene (4.4 GB) larger than L2",
                        "mean_ray_stats": {"marching": round(float(mean_stats[0]), 2),
                                           "occupied": round(float(mean_stats[1]), 2),
@@ -604,7 +623,12 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "kernel": "march_kernel (K1)",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bytes_k1 / args.steps,
-                         "l2_traffic": l2_traffic, "other_ceilings": ceilings},
+                         "l2_traffic": l2_traffic, "other_ceilings": ceilings,
+                         # measured bytes (ncu, same build, profiles/ncu_traffic.json) over
+                         # this run's K1 event time, and the ceiling that binds
+                         "l2_gbs": (l2_traffic / (k1_avg / 1e3) / 1e9) if l2_traffic else None,
+                         "dram_gbs": (traffic / (k1_avg / 1e3) / 1e9) if traffic else None,
+                         "binding_ceiling": binding_ceiling(l2_traffic, traffic, k1_avg, ceilings)},
             "k2_tensor": {"kernel": "shade_tc_kernel (K2)" if args.mlp == "tensor" else "shade_exact_kernel",
                           "shaded_rays": int(shaded), "flop_per_launch": k2_flop,
                           "achieved_tflops": k2_flop / (k2_avg * 1e-3) / 1e12,

@@ -116,6 +116,9 @@ struct ngprt_scene {
             if (r) cudaStreamDestroy(r);
         if (async.copy) cudaStreamDestroy(async.copy);
         for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
+        // the fine tables' persisting L2 lines would otherwise outlive the scene
+        // (normal-access writes cannot evict them)
+        if (fine_block) cudaCtxResetPersistingL2Cache();
         for (void* p : allocs) cudaFree(p);
         cudaSetDevice(prev);
     }

@@ -7,9 +7,13 @@ run --config c2_blob800
 run --config c2_blob800 --batch 50
 run --config c3_1080p
 run --config c3_1080p --mlp exact
+run --config c3_1080p_f32
+run --config c3_mip360
+run --config c3_1080p --shard tiles
 run --config c4_1080p_x64
 run --config c4_1080p_x64 --batch 64
 for nb in 10 35 140 560 2240; do run --config c5_2160p --scene n_boxes=$nb; done
+run --config c5_2160p --shard tiles
 python - <<'PY' $out
 import json,sys
 for l in open(sys.argv[1]):

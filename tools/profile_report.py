@@ -23,10 +23,13 @@ PROF = ROOT / "profiles"
 CONFIG_NAMES = ["c1_256 (256x256, L=4, 2^19, bench, 256^3/128^3 DT)",
                 "c2_blob800 (800x800, L=2, 2^22, blob), one frame per call",
                 "c2_blob800, 100-camera orbit as 2 calls of 50 cameras",
-                "c3_1080p (1920x1080, L=2, 2^21, mip360)", "c3_1080p, exact CUDA-core MLP",
+                "c3_1080p (1920x1080, L=2, 2^21, mip360c calibrated)", "c3_1080p, exact CUDA-core MLP",
+                "c3_1080p_f32 (f32 storage)", "c3_mip360 (round-1 preset)",
+                "c3_1080p, --shard tiles (N=1: one tile-major launch + assemble)",
                 "c4_1080p_x64 (per-frame, camera ring)",
                 "c4_1080p_x64, 64 cameras per call"] + \
-               [f"c5_2160p boxes={n} (3840x2160, L=2, 2^22)" for n in (10, 35, 140, 560, 2240)]
+               [f"c5_2160p boxes={n} (3840x2160, L=2, 2^22)" for n in (10, 35, 140, 560, 2240)] + \
+               ["c5_2160p boxes=140, --shard tiles"]
 
 
 def regions(tsv: Path, src: Path):
