@@ -4,6 +4,7 @@
 // a message for ngprt_last_error() (the reference throws, e.g. baking.hpp:396-405).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -186,10 +187,40 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
     }
     const uint64_t r1c = uint64_t(d->L_C) + 1;
     const uint64_t n_corner = r1c * r1c * r1c;
-    for (uint64_t i = 0; i < d->n_coarse; ++i)
-        if (d->coarse_keys[i] >= n_corner)
-            return fail(NGPRT_EINVAL, "coarse key " + std::to_string(d->coarse_keys[i]) +
-                                          " outside the (L_C+1)^3 corner grid");
+    // Keys must be in range. A repeated key keeps its FIRST row, as the reference's
+    // SparseCoarseGrid::add_row does (index.emplace ignores a second insert,
+    // baking.hpp:33-38); later duplicates are dropped on the host so the device
+    // scatter never writes one corner twice.
+    std::vector<uint64_t> dedup_keys;
+    std::vector<float> dedup_rows;
+    const uint64_t* coarse_keys = d->coarse_keys;
+    const float* coarse_rows = d->coarse_rows;
+    uint64_t n_coarse = d->n_coarse;
+    {
+        std::vector<uint64_t> seen(d->n_coarse ? (n_corner + 63) / 64 : 0, 0);
+        bool dup = false;
+        for (uint64_t i = 0; i < d->n_coarse; ++i) {
+            const uint64_t k = d->coarse_keys[i];
+            if (k >= n_corner)
+                return fail(NGPRT_EINVAL, "coarse key " + std::to_string(k) +
+                                              " outside the (L_C+1)^3 corner grid");
+            dup |= (seen[k >> 6] >> (k & 63)) & 1;
+            seen[k >> 6] |= uint64_t(1) << (k & 63);
+        }
+        if (dup) {
+            std::fill(seen.begin(), seen.end(), 0);
+            for (uint64_t i = 0; i < d->n_coarse; ++i) {
+                const uint64_t k = d->coarse_keys[i];
+                if ((seen[k >> 6] >> (k & 63)) & 1) continue;
+                seen[k >> 6] |= uint64_t(1) << (k & 63);
+                dedup_keys.push_back(k);
+                dedup_rows.insert(dedup_rows.end(), d->coarse_rows + i * w, d->coarse_rows + (i + 1) * w);
+            }
+            coarse_keys = dedup_keys.data();
+            coarse_rows = dedup_rows.data();
+            n_coarse = dedup_keys.size();
+        }
+    }
     if (d->dist_res) {
         bool ok = d->dist_values != nullptr;
         for (int k = 0; k < NGPRT_PYRAMID_LEVELS; ++k)
@@ -224,8 +255,8 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
                   : std::strcmp(e, "f16") == 0 ? NGPRT_STORAGE_F16 : storage;
     if (storage == NGPRT_STORAGE_AUTO) {
         bool exact = true;
-        for (uint64_t i = 0; exact && i < d->n_coarse * uint64_t(w); ++i)
-            exact = fp16_exact(d->coarse_rows[i]);
+        for (uint64_t i = 0; exact && i < n_coarse * uint64_t(w); ++i)
+            exact = fp16_exact(coarse_rows[i]);
         for (int l = 0; exact && l < L; ++l)
             for (uint64_t i = 0; exact && i < d->fine_table_len[l] * 8; ++i)
                 exact = fp16_exact(d->fine_tables[l][i]);
@@ -271,14 +302,14 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         NG_TRY(s->alloc(&dense, bytes));
         NG_TRY(cudaMemsetAsync(dense, 0, bytes, st));
         s->info.coarse_bytes = bytes;
-        if (d->n_coarse) {
+        if (n_coarse) {
             unsigned long long* dkeys;
             float* drows;
-            NG_TRY(cudaMallocAsync(&dkeys, d->n_coarse * 8, st));
-            NG_TRY(cudaMallocAsync(&drows, d->n_coarse * w * 4, st));
-            NG_TRY(cudaMemcpyAsync(dkeys, d->coarse_keys, d->n_coarse * 8, cudaMemcpyHostToDevice, st));
-            NG_TRY(cudaMemcpyAsync(drows, d->coarse_rows, d->n_coarse * w * 4, cudaMemcpyHostToDevice, st));
-            launch_scatter_coarse(dkeys, drows, d->n_coarse, w, dense, f16, st);
+            NG_TRY(cudaMallocAsync(&dkeys, n_coarse * 8, st));
+            NG_TRY(cudaMallocAsync(&drows, n_coarse * w * 4, st));
+            NG_TRY(cudaMemcpyAsync(dkeys, coarse_keys, n_coarse * 8, cudaMemcpyHostToDevice, st));
+            NG_TRY(cudaMemcpyAsync(drows, coarse_rows, n_coarse * w * 4, cudaMemcpyHostToDevice, st));
+            launch_scatter_coarse(dkeys, drows, n_coarse, w, dense, f16, st);
             NG_TRY(cudaGetLastError());
             NG_TRY(cudaFreeAsync(dkeys, st));
             NG_TRY(cudaFreeAsync(drows, st));

@@ -26,7 +26,7 @@ struct Reader {  // detail::ByteReader, training.hpp:464-479
     const unsigned char* p;
     size_t len, off = 0;
     void read(void* dst, size_t n, const char* what) {
-        if (off + n > len)
+        if (n > len - off)  // off <= len always; no wrap for huge n
             throw std::runtime_error(std::string("checkpoint: truncated reading ") + what +
                                      " at offset " + std::to_string(off));
         std::memcpy(dst, p + off, n);
@@ -42,6 +42,7 @@ struct Reader {  // detail::ByteReader, training.hpp:464-479
 
 void read_mlp(Reader& pr, const char* tag, std::vector<float>* w, std::vector<float>* b) {
     const uint32_t nd = pr.pod<uint32_t>("mlp ndims");
+    if (nd > 16) throw std::runtime_error(std::string("load_baked: ") + tag + " has too many layers");
     std::vector<int> dims(nd);
     for (auto& d : dims) d = int(pr.pod<uint32_t>("mlp dim"));
     const std::vector<int> want = {23, 64, 64, 3};  // shade requires 23 -> 3 (volume.hpp:121-122)
@@ -93,7 +94,14 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
         for (uint32_t l = 0; l < L; ++l) {
             d.fine_table_len[l] = lens[kCoarseLevels + l];
             d.fine_hashed[l] = 1;  // load_baked: Addressing::Hashed (baking.hpp:384)
+            // bounds the reference leaves unchecked: a crafted length would make the
+            // section-2 size arithmetic wrap and the device hash read out of bounds
+            if (d.fine_table_len[l] == 0 || d.fine_table_len[l] > (uint64_t(1) << 32))
+                throw std::runtime_error("load_baked: fine table length out of range (1..2^32)");
+            if (d.fine_res[l] == 0 || d.fine_res[l] > (1u << 20))
+                throw std::runtime_error("load_baked: fine resolution out of range (1..2^20)");
         }
+        if (lc == 0 || lc > 4096) throw std::runtime_error("load_baked: L_C out of range (1..4096)");
         d.fusion_tag = r.pod<uint8_t>("fusion tag");
         while ((r.off - header_start) % 8 != 0) r.pod<uint8_t>("pad");
         const int w = 8 + 2 * int(L);
@@ -103,7 +111,7 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
             const size_t sec_off = r.off;
             const uint32_t id = r.pod<uint32_t>("section id");
             const uint64_t len = r.pod<uint64_t>("section length");
-            if (r.off + len + 4 > r.len)
+            if (len > r.len - r.off || r.len - r.off - len < 4)  // no u64 wrap
                 throw std::runtime_error("load_baked: truncated section " + std::to_string(id) +
                                          " at offset " + std::to_string(sec_off));
             const unsigned char* payload = r.p + r.off;
@@ -117,6 +125,9 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
             switch (id) {
                 case 1: {  // coarse corner map, sorted by key
                     const uint64_t count = pr.pod<uint64_t>("corner count");
+                    if (count > (pr.len - pr.off) / (8 + sizeof(float) * w))
+                        throw std::runtime_error("load_baked: corner count exceeds section 1 at offset " +
+                                                 std::to_string(sec_off));
                     b->keys.resize(count);
                     b->rows.resize(count * w);
                     for (uint64_t i = 0; i < count; ++i) {
@@ -125,12 +136,18 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
                     }
                     break;
                 }
-                case 2:
+                case 2: {
+                    uint64_t want = 0;
+                    for (uint32_t l = 0; l < L; ++l) want += d.fine_table_len[l] * 32;
+                    if (want != len)
+                        throw std::runtime_error("load_baked: fine table section size mismatch at offset " +
+                                                 std::to_string(sec_off));
                     for (uint32_t l = 0; l < L; ++l) {
                         b->fine[l].resize(d.fine_table_len[l] * 8);
                         pr.read(b->fine[l].data(), b->fine[l].size() * 4, "fine table");
                     }
                     break;
+                }
                 case 3:
                     read_mlp(pr, "view MLP", b->psi_w, b->psi_b);
                     break;
@@ -151,6 +168,7 @@ ngprt_status ngprt_baked_load(const char* path, ngprt_baked** out) {
                     break;
                 case 7: {  // fusion MLP {8L, 64, 8} (baking.hpp:452-466)
                     const uint32_t nd = pr.pod<uint32_t>("fusion mlp ndims");
+                    if (nd > 16) throw std::runtime_error("load_baked: fusion MLP has too many layers");
                     std::vector<int> dims(nd);
                     for (auto& dd : dims) dd = int(pr.pod<uint32_t>("fusion mlp dim"));
                     if (dims != std::vector<int>{8 * int(L), 64, 8})

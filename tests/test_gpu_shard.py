@@ -183,3 +183,30 @@ def test_concurrent_renders_from_host_threads(ng, torch, small):
     for (which, k, rep, i), r in got.items():
         ref = want[i] if which == "a" else want_o[i]
         assert np.array_equal(r.numpy().view(np.uint32), ref.numpy().view(np.uint32)), (which, k, i)
+
+
+def test_duplicate_coarse_keys_keep_the_first_row(ng, torch):
+    """A descriptor that repeats coarse keys: the first row of each key wins, as
+    the reference's SparseCoarseGrid::add_row (index.emplace) keeps it; the
+    render equals the compiled reference on the same descriptor bit for bit."""
+    import ctypes as C
+    from checkers import CpuScene
+    synth = ng.SynthScene(occupancy="bench", occ_base_res=64, L=2, L_C=64, fine_table_len=1 << 12)
+    keys, rows = synth.coarse_keys(), synth.coarse_rows()
+    rng = np.random.RandomState(1)
+    pick = rng.choice(len(keys), 500, replace=False)
+    k2 = np.ascontiguousarray(np.concatenate([keys, keys[pick]]))
+    r2 = np.ascontiguousarray(np.concatenate([rows, rows[pick] * 3.0 + 1.0]).astype(np.float32))
+    d = ng._abi.SceneDesc.from_buffer_copy(synth.desc)
+    d.n_coarse = len(k2)
+    d.coarse_keys = k2.ctypes.data_as(C.POINTER(C.c_uint64))
+    d.coarse_rows = r2.ctypes.data_as(C.POINTER(C.c_float))
+    cam = ng.cameras(3, 64, 48)[2]
+    dup = ng.Scene(d)
+    rgb, st = ng.render(dup, [cam], ng.Opts(mlp="exact"), stats=True)
+    want_rgb, want_st = CpuScene(C.pointer(d), "ref").render(cam, ng.Opts(mlp="exact").to_c())
+    base = ng.render(ng.Scene(synth), [cam], ng.Opts(mlp="exact"))
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(rgb[0]), want_rgb.view(np.uint32))
+    assert np.array_equal(st[0].cpu().numpy().view(np.uint32), want_st)
+    assert np.array_equal(bits(rgb), bits(base))

@@ -82,6 +82,37 @@ def test_corrupt_files_fail_like_the_reference(ng, saved, tmp_path):
         ng.BakedFile(tmp_path / "missing.ngrt")
 
 
+def test_crafted_lengths_are_rejected(ng, saved, tmp_path):
+    """Header / section lengths the reference never bounds (baking.hpp:396-405):
+    a section length near 2^64 (the end-of-section test would wrap), a fine
+    table length that would make the section-2 arithmetic wrap, and a section 2
+    whose size does not match the table lengths all fail with a message."""
+    import struct
+    _, _, path = saved
+    data = bytearray(path.read_bytes())
+    # header: "NGRT", u32 version, u32 L_C, u32 L, u32 fine_res[2], u64 lens[6 + 2], u8 tag, pad
+    first_section = 8 + ((4 + 4 + 8 + 64 + 1 + 7) // 8) * 8
+    assert struct.unpack_from("<I", data, first_section)[0] == 1
+    wrap = bytearray(data)
+    struct.pack_into("<Q", wrap, first_section + 4, (1 << 64) - 8)
+    p = tmp_path / "wrap.ngrt"
+    p.write_bytes(bytes(wrap))
+    with pytest.raises(ng.NgprtError, match="truncated section 1"):
+        ng.BakedFile(p)
+    huge = bytearray(data)
+    struct.pack_into("<Q", huge, 8 + 16 + 6 * 8, 1 << 61)  # fine level 0 table length
+    p = tmp_path / "huge.ngrt"
+    p.write_bytes(bytes(huge))
+    with pytest.raises(ng.NgprtError, match="fine table length out of range"):
+        ng.BakedFile(p)
+    small = bytearray(data)
+    struct.pack_into("<Q", small, 8 + 16 + 6 * 8, 1 << 11)  # half the stored rows
+    p = tmp_path / "small.ngrt"
+    p.write_bytes(bytes(small))
+    with pytest.raises(ng.NgprtError, match="fine table section size mismatch"):
+        ng.BakedFile(p)
+
+
 @pytest.mark.gpu
 def test_loaded_file_renders_like_the_reference(ng, saved):
     import torch
