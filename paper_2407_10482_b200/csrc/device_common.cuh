@@ -8,6 +8,7 @@
 
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <stdio.h>  // device printf of the NGPRT_DEBUG_BOUNDS checks
 
 #include "ngprt_cuda.h"
 
@@ -106,6 +107,27 @@ __device__ __forceinline__ void sh_encode(float x, float y, float z, float* out)
 // ---------------------------------------------------------------------------
 // Scene as seen by the kernels (built by ngprt_scene_create).
 // ---------------------------------------------------------------------------
+// Device-side bounds assertions on every gather and per-ray store
+// (NGPRT_DEBUG_BOUNDS=1 build variant, tools/build_variant.py; compiled out
+// otherwise). They stand in for compute-sanitizer, which this GPU pool does not
+// allow: tests/test_gpu_bounds.py renders the parity cases with the variant.
+#ifndef NGPRT_DEBUG_BOUNDS
+#define NGPRT_DEBUG_BOUNDS 0
+#endif
+#if NGPRT_DEBUG_BOUNDS
+#define NG_BOUNDS(cond)                                                                 \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("ngprt bounds check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define NG_BOUNDS(cond) \
+    do {                \
+    } while (0)
+#endif
+
 struct DevScene {
     int L;
     int L_C;

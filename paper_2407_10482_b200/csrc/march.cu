@@ -386,9 +386,11 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
         } else
 #endif
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            load_fine_row<F16>(table, (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask,
-                               frow[k]);
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t row = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
+            NG_BOUNDS(row < sc.fine_len[l]);
+            load_fine_row<F16>(table, row, frow[k]);
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             fine[0] = mac(false, fine[0], w[k], frow[k][0]);
@@ -404,7 +406,9 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
             const float wk = ((dx ? f[0] : 1.0f - f[0]) * (dy ? f[1] : 1.0f - f[1])) *
                              (dz ? f[2] : 1.0f - f[2]);
             float row[8];
-            load_fine_row<F16>(table, fine_index(sc, l, b[0] + dx, b[1] + dy, b[2] + dz), row);
+            const unsigned long long fi = fine_index(sc, l, b[0] + dx, b[1] + dy, b[2] + dz);
+            NG_BOUNDS(fi < sc.fine_len[l]);
+            load_fine_row<F16>(table, fi, row);
 #pragma unroll
             for (int c = 0; c < 8; ++c) fine[c] = mac(FC && c != 0, fine[c], wk, row[c]);
         }
@@ -441,10 +445,11 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
             const uint32_t sy = r1, sz = r1 * r1;
             float rows[8][W];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                load_coarse_row<W, F16>(sc.coarse,
-                                        key0 + (k & 1) + ((k >> 1) & 1) * sy + (k >> 2) * sz,
-                                        rows[k]);
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t key = key0 + (k & 1) + ((k >> 1) & 1) * sy + (k >> 2) * sz;
+                NG_BOUNDS(key < uint64_t(r1) * r1 * r1);
+                load_coarse_row<W, F16>(sc.coarse, key, rows[k]);
+            }
 #pragma unroll
             for (int k = 0; k < 8; ++k)
 #pragma unroll
@@ -458,6 +463,7 @@ __device__ __forceinline__ void decode_point(const DevScene& sc, const float x[3
                     R1 * ((unsigned long long)(cb[1] + ((k >> 1) & 1)) +
                           R1 * (unsigned long long)(cb[2] + (k >> 2)));
                 float row[W];
+                NG_BOUNDS(key < R1 * R1 * R1);
                 load_coarse_row<W, F16>(sc.coarse, key, row);
                 const float wk = (((k & 1) ? cf[0] : 1.0f - cf[0]) *
                                   (((k >> 1) & 1) ? cf[1] : 1.0f - cf[1])) *
@@ -611,6 +617,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const uint32_t key = key0 + (k & 1) + ((k >> 1) & 1) * r1 + (k >> 2) * r1 * r1;
+        NG_BOUNDS(key < uint64_t(r1) * r1 * r1);
         const uint4* p = reinterpret_cast<const uint4*>(sc.coarse) + size_t(key) * 2;
         if constexpr (!F16) {
             load_coarse_f32_raw<W>(sc.coarse, key, craw[k]);
@@ -641,7 +648,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         const uint32_t s0 = uint32_t(__cvta_generic_to_shared(stage + j * 8 * kBlock));
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const uint4* src = table + ((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask);
+            const uint32_t row = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
+            NG_BOUNDS(row < sc.fine_len[l]);
+            const uint4* src = table + row;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;"
                          :: "r"(s0 + uint32_t(k * kBlock * 16)), "l"(src) : "memory");
         }
@@ -668,6 +677,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const uint32_t row = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
+            NG_BOUNDS(row < sc.fine_len[l]);
             if constexpr (F16) {
                 const uint4 v = ldg_fine(table + row);
                 fraw[l][k][0] = v.x; fraw[l][k][1] = v.y; fraw[l][k][2] = v.z; fraw[l][k][3] = v.w;
@@ -881,6 +891,7 @@ __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s
     r.c = make_float4(valid ? s.ray.d[0] : 0.f, valid ? s.ray.d[1] : 0.f,
                       valid ? s.ray.d[2] : 0.f, valid ? 1.f : 0.f);
     const uint32_t idx = s.out_idx & kIdxMask;
+    NG_BOUNDS(idx < p.n_slots);
     p.acc[idx] = r;
     if (p.stats) {
         ngprt_ray_stats st;
@@ -916,6 +927,7 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
         if (px >= p.w || py >= p.h) return;
         s.out_idx = (cam * p.h + py) * p.w + px;
     }
+    NG_BOUNDS(s.out_idx < p.n_slots);
     const float4 a = __ldg(p.rays + 2 * size_t(s.out_idx));
     const float4 b = __ldg(p.rays + 2 * size_t(s.out_idx) + 1);
     if (!(b.w >= 0.0f)) return;  // K0 wrote the result (generate_rays/clip_to_roi miss)
@@ -983,6 +995,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     for (int a = 0; a < 3; ++a) i0[a] = voxel_1d_clamped(xc[a], sc.occ_h0, r0);
     // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
     const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
+    NG_BOUNDS(pidx < uint32_t(r1) * uint32_t(r1) * uint32_t(r1));
     const uint32_t code = ldg_probe(sc.probe + pidx);
     // occupancy_probe counters: e + 1 levels read (5 when level 0 decides).
     // Written branch-free so every empty point reaches next_step on one path.
@@ -1018,7 +1031,9 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
             const int vx = voxel_1d_clamped(xc[0], sc.dist_h, gr),
                       vy = voxel_1d_clamped(xc[1], sc.dist_h, gr),
                       vz = voxel_1d_clamped(xc[2], sc.dist_h, gr);
-            g = __ldg(sc.dist + (size_t(vx) + size_t(gr) * (size_t(vy) + size_t(gr) * vz)));
+            const size_t di = size_t(vx) + size_t(gr) * (size_t(vy) + size_t(gr) * vz);
+            NG_BOUNDS(di < size_t(gr) * gr * gr);
+            g = __ldg(sc.dist + di);
         }
     }
     float step;
@@ -1275,6 +1290,7 @@ __global__ void __launch_bounds__(256) raygen_kernel(const MarchParams p) {
         if (px >= p.w || py >= p.h) return;
         idx = (uint32_t(cam) * p.h + py) * p.w + px;
     }
+    NG_BOUNDS(idx < p.n_slots);
     Ray r;
     const bool valid = generate_ray(p.cams[cam], double(p.x0 + px) + 0.5, double(p.y0 + py) + 0.5, r);
     float t0 = 0.f, t1 = -1.0f;

@@ -635,6 +635,7 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
     for (int c0 = 0; c0 < n_cams; c0 += cams_per_launch) {
         const int nc = std::min(cams_per_launch, n_cams - c0);
         p.n_cams = nc;
+        p.n_slots = uint32_t(per_cam * nc);
         for (int i = 0; i < nc; ++i) {
             const ngprt_camera& cam = cams[c0 + i];
             CamParams& cp = p.cams[i];

@@ -10,8 +10,9 @@
 // separable min-max transform instead of the reference's serial two-pass
 // chamfer (which has a loop-carried dependency over the whole grid):
 //   D(p) = min_qz max(|pz-qz|, min_qy max(|py-qy|, min_qx |px-qx|)).
-// Pass X is a two-sweep 1-D distance per row; passes Y and Z search outward
-// with early exit (a candidate at offset k is >= k).
+// Pass X is a two-sweep 1-D distance per row (one warp per row, ballots);
+// passes Y and Z take the lower envelope of max(|u - i|, g(i)) per column in
+// O(r) (NGPRT_DT_SEARCH: the earlier outward search with early exit).
 #include "render.cuh"
 
 namespace ngprt_dev {
@@ -39,7 +40,49 @@ __global__ void pyramid_kernel(const uint32_t* __restrict__ src, int rs, uint32_
     if ((threadIdx.x & 31) == 0 && i < n) dst[i >> 5] = m;
 }
 
-// Pass X: per row (y, z), distance to the nearest occupied voxel along x.
+// Pass X: per row (y, z), distance to the nearest occupied voxel along x. One
+// warp per row, 32 voxels per step: a ballot of the occupancy bits gives, per
+// lane, the nearest set bit at or before it inside the step (a masked clz) and a
+// warp-uniform carry of the last set bit of earlier steps; a backward sweep does
+// the same for the nearest set bit after. Loads and u16 stores are coalesced
+// (64 B per warp store).
+__global__ void dt_x_warp_kernel(const uint32_t* __restrict__ occ, int r, uint16_t* __restrict__ out) {
+    const size_t row = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (row >= size_t(r) * r) return;  // warp-uniform
+    const size_t base = row * size_t(r);
+    uint16_t* o = out + base;
+    const int groups = (r + 31) / 32;
+    int last = -1;  // last occupied x before the current group (warp-uniform)
+    for (int g = 0; g < groups; ++g) {
+        const int x = g * 32 + int(lane);
+        const size_t i = base + size_t(x);
+        const bool in = x < r;
+        const bool bit = in && ((occ[i >> 5] >> (i & 31)) & 1u);
+        const uint32_t m = __ballot_sync(0xffffffffu, bit);
+        const uint32_t le = m & (0xffffffffu >> (31u - lane));  // bits at or before lane
+        const int prev = le ? g * 32 + 31 - __clz(le) : last;
+        if (in) o[x] = prev < 0 ? kInf : uint16_t(min(x - prev, int(kInf)));
+        if (m) last = g * 32 + 31 - __clz(m);
+    }
+    int next = -1;  // first occupied x after the current group
+    for (int g = groups - 1; g >= 0; --g) {
+        const int x = g * 32 + int(lane);
+        const size_t i = base + size_t(x);
+        const bool in = x < r;
+        const bool bit = in && ((occ[i >> 5] >> (i & 31)) & 1u);
+        const uint32_t m = __ballot_sync(0xffffffffu, bit);
+        const uint32_t ge = m & (0xffffffffu << lane);  // bits at or after lane
+        const int nx = ge ? g * 32 + __ffs(ge) - 1 : next;
+        if (in && nx >= 0) {
+            const uint16_t d = uint16_t(min(nx - x, int(kInf)));
+            if (d < o[x]) o[x] = d;
+        }
+        if (m) next = g * 32 + __ffs(m) - 1;
+    }
+}
+
+// Pass X, one thread per row (the first version; kept for NGPRT_DT_X_SERIAL A/B).
 __global__ void dt_x_kernel(const uint32_t* __restrict__ occ, int r, uint16_t* __restrict__ out) {
     const size_t row = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     if (row >= size_t(r) * r) return;
@@ -87,6 +130,74 @@ __global__ void dt_minmax_kernel(const uint16_t* __restrict__ in, int r, uint16_
     }
 }
 
+// Passes Y and Z in O(r) per column: the lower envelope of the functions
+// f_i(u) = max(|u - i|, g(i)) over the column (Meijster, Roerdink & Hesselink's
+// separable transform with its chessboard-metric separator), one thread per
+// column; consecutive threads take consecutive x, so every load and store of the
+// sweep is coalesced. The envelope stacks (s: function index, t: start of its
+// interval) live in the thread's local memory (L1). Exact integer arithmetic:
+// the same grid as the early-exit search above and the reference's chamfer.
+__device__ __forceinline__ int cheb_f(int u, int i, int gi) {
+    const int d = u > i ? u - i : i - u;
+    return d > gi ? d : gi;
+}
+__device__ __forceinline__ int cheb_sep(int i, int u, int gi, int gu) {
+    const int mid = (i + u) >> 1;  // i < u, both >= 0: floor
+    if (gi <= gu) return (i + gu) > mid ? (i + gu) : mid;
+    return (u - gi) < mid ? (u - gi) : mid;
+}
+template <int AXIS, bool FINAL, int NMAX>
+__global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restrict__ in, int r,
+                                                         uint16_t* __restrict__ out,
+                                                         uint8_t* __restrict__ out8) {
+    const size_t col = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (col >= size_t(r) * r) return;
+    // AXIS 1 (y): column (x, z), element u at (z * r + u) * r + x
+    // AXIS 2 (z): column (x, y), element u at (u * r + y) * r + x
+    const size_t x = col % size_t(r), o = col / size_t(r);
+    const size_t base = AXIS == 1 ? o * size_t(r) * r + x : o * size_t(r) + x;
+    const size_t stride = AXIS == 1 ? size_t(r) : size_t(r) * r;
+    uint16_t s[NMAX], t[NMAX];  // NMAX >= r
+    int q = 0;
+    s[0] = 0;
+    t[0] = 0;
+    int gs = in[base];  // g(s[q]), kept in a register
+    for (int u = 1; u < r; ++u) {
+        const int gu = in[base + size_t(u) * stride];
+        while (q >= 0 && cheb_f(t[q], s[q], gs) > cheb_f(t[q], u, gu)) {
+            --q;
+            if (q >= 0) gs = in[base + size_t(s[q]) * stride];
+        }
+        if (q < 0) {
+            q = 0;
+            s[0] = uint16_t(u);
+            gs = gu;
+        } else {
+            const int w = 1 + cheb_sep(s[q], u, gs, gu);
+            if (w < r) {
+                ++q;
+                s[q] = uint16_t(u);
+                t[q] = uint16_t(w);
+                gs = gu;
+            }
+        }
+    }
+    for (int u = r - 1; u >= 0; --u) {
+        const int h = cheb_f(u, s[q], gs);
+        const size_t i = base + size_t(u) * stride;
+        if (FINAL) {
+            const int g = h == 0 ? 0 : h - 1;  // occupancy.hpp:188-192
+            out8[i] = uint8_t(g < 255 ? g : 255);
+        } else {
+            out[i] = uint16_t(h < int(kInf) ? h : int(kInf));
+        }
+        if (u == t[q] && q > 0) {
+            --q;
+            gs = in[base + size_t(s[q]) * stride];
+        }
+    }
+}
+
 template <bool F16>
 __global__ void scatter_coarse_kernel(const unsigned long long* __restrict__ keys,
                                       const float* __restrict__ rows, size_t n, int w,
@@ -123,9 +234,26 @@ void launch_pyramid_level(const uint32_t* src, int src_res, uint32_t* dst, cudaS
 void launch_distance_grid(const uint32_t* occ, int r, uint16_t* a, uint16_t* b, uint8_t* out,
                           cudaStream_t st) {
     const size_t rows = size_t(r) * r, n = rows * r;
+#ifdef NGPRT_DT_X_SERIAL
     dt_x_kernel<<<blocks_for(rows, 128), 128, 0, st>>>(occ, r, a);
+#else
+    dt_x_warp_kernel<<<blocks_for(rows * 32, 256), 256, 0, st>>>(occ, r, a);
+#endif
+#ifdef NGPRT_DT_SEARCH
     dt_minmax_kernel<1, false><<<blocks_for(n, 256), 256, 0, st>>>(a, r, b, nullptr);
     dt_minmax_kernel<2, true><<<blocks_for(n, 256), 256, 0, st>>>(b, r, nullptr, out);
+#else
+    if (r <= 256) {
+        dt_envelope_kernel<1, false, 256><<<blocks_for(rows, 64), 64, 0, st>>>(a, r, b, nullptr);
+        dt_envelope_kernel<2, true, 256><<<blocks_for(rows, 64), 64, 0, st>>>(b, r, nullptr, out);
+    } else if (r <= 1024) {
+        dt_envelope_kernel<1, false, 1024><<<blocks_for(rows, 64), 64, 0, st>>>(a, r, b, nullptr);
+        dt_envelope_kernel<2, true, 1024><<<blocks_for(rows, 64), 64, 0, st>>>(b, r, nullptr, out);
+    } else {  // beyond the envelope stacks' size: the outward search
+        dt_minmax_kernel<1, false><<<blocks_for(n, 256), 256, 0, st>>>(a, r, b, nullptr);
+        dt_minmax_kernel<2, true><<<blocks_for(n, 256), 256, 0, st>>>(b, r, nullptr, out);
+    }
+#endif
 }
 
 void launch_scatter_coarse(const unsigned long long* keys, const float* rows, size_t n, int w,

@@ -60,6 +60,7 @@ struct MarchParams {
     ngprt_ray_stats* stats;   // nullable, n_cams x h x w
     unsigned int* work;       // tile counter (zeroed before launch)
     const float4* rays;       // K0 -> K1: (o, t0), (d, t1) per ray; t1 < 0 = already finished
+    uint32_t n_slots;         // rays / acc / stats entries of this launch (bounds checks)
 };
 
 // K1: march + gather + fuse + composite. Persistent warps, one ray per lane,
