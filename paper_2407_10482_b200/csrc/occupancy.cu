@@ -146,27 +146,35 @@ __device__ __forceinline__ int cheb_sep(int i, int u, int gi, int gu) {
     if (gi <= gu) return (i + gu) > mid ? (i + gu) : mid;
     return (u - gi) < mid ? (u - gi) : mid;
 }
+// The column is first staged in shared memory (independent coalesced loads, all
+// in flight at once), so the sequential envelope sweep reads no global memory.
 template <int AXIS, bool FINAL, int NMAX>
 __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restrict__ in, int r,
                                                          uint16_t* __restrict__ out,
                                                          uint8_t* __restrict__ out8) {
-    const size_t col = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (col >= size_t(r) * r) return;
+    extern __shared__ uint16_t colbuf[];  // [r][blockDim.x]
+    const int C = blockDim.x, tid = threadIdx.x;
+    const size_t col = blockIdx.x * size_t(C) + tid;
+    const bool live = col < size_t(r) * r;
     // AXIS 1 (y): column (x, z), element u at (z * r + u) * r + x
     // AXIS 2 (z): column (x, y), element u at (u * r + y) * r + x
     const size_t x = col % size_t(r), o = col / size_t(r);
     const size_t base = AXIS == 1 ? o * size_t(r) * r + x : o * size_t(r) + x;
     const size_t stride = AXIS == 1 ? size_t(r) : size_t(r) * r;
-    uint16_t s[NMAX], t[NMAX];  // NMAX >= r
+    if (!live) return;  // no block-wide synchronisation below: each thread owns its column
+    uint16_t* g = colbuf + tid;
+#pragma unroll 8
+    for (int u = 0; u < r; ++u) g[u * C] = in[base + size_t(u) * stride];
+    uint16_t s[NMAX], t[NMAX];  // NMAX >= r: envelope stacks (local memory, L1)
     int q = 0;
     s[0] = 0;
     t[0] = 0;
-    int gs = in[base];  // g(s[q]), kept in a register
+    int gs = g[0];  // g(s[q]), kept in a register
     for (int u = 1; u < r; ++u) {
-        const int gu = in[base + size_t(u) * stride];
+        const int gu = g[u * C];
         while (q >= 0 && cheb_f(t[q], s[q], gs) > cheb_f(t[q], u, gu)) {
             --q;
-            if (q >= 0) gs = in[base + size_t(s[q]) * stride];
+            if (q >= 0) gs = g[s[q] * C];
         }
         if (q < 0) {
             q = 0;
@@ -186,14 +194,14 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
         const int h = cheb_f(u, s[q], gs);
         const size_t i = base + size_t(u) * stride;
         if (FINAL) {
-            const int g = h == 0 ? 0 : h - 1;  // occupancy.hpp:188-192
-            out8[i] = uint8_t(g < 255 ? g : 255);
+            const int gg = h == 0 ? 0 : h - 1;  // occupancy.hpp:188-192
+            out8[i] = uint8_t(gg < 255 ? gg : 255);
         } else {
             out[i] = uint16_t(h < int(kInf) ? h : int(kInf));
         }
         if (u == t[q] && q > 0) {
             --q;
-            gs = in[base + size_t(s[q]) * stride];
+            gs = g[s[q] * C];
         }
     }
 }
@@ -243,12 +251,14 @@ void launch_distance_grid(const uint32_t* occ, int r, uint16_t* a, uint16_t* b, 
     dt_minmax_kernel<1, false><<<blocks_for(n, 256), 256, 0, st>>>(a, r, b, nullptr);
     dt_minmax_kernel<2, true><<<blocks_for(n, 256), 256, 0, st>>>(b, r, nullptr, out);
 #else
-    if (r <= 256) {
-        dt_envelope_kernel<1, false, 256><<<blocks_for(rows, 64), 64, 0, st>>>(a, r, b, nullptr);
-        dt_envelope_kernel<2, true, 256><<<blocks_for(rows, 64), 64, 0, st>>>(b, r, nullptr, out);
-    } else if (r <= 1024) {
-        dt_envelope_kernel<1, false, 1024><<<blocks_for(rows, 64), 64, 0, st>>>(a, r, b, nullptr);
-        dt_envelope_kernel<2, true, 1024><<<blocks_for(rows, 64), 64, 0, st>>>(b, r, nullptr, out);
+    if (r <= 256) {  // 64 columns x r x 2 B of staging per CTA (<= 32 KB)
+        const size_t sm = size_t(r) * 64 * 2;
+        dt_envelope_kernel<1, false, 256><<<blocks_for(rows, 64), 64, sm, st>>>(a, r, b, nullptr);
+        dt_envelope_kernel<2, true, 256><<<blocks_for(rows, 64), 64, sm, st>>>(b, r, nullptr, out);
+    } else if (r <= 1024) {  // 16 columns per CTA (<= 32 KB)
+        const size_t sm = size_t(r) * 16 * 2;
+        dt_envelope_kernel<1, false, 1024><<<blocks_for(rows, 16), 16, sm, st>>>(a, r, b, nullptr);
+        dt_envelope_kernel<2, true, 1024><<<blocks_for(rows, 16), 16, sm, st>>>(b, r, nullptr, out);
     } else {  // beyond the envelope stacks' size: the outward search
         dt_minmax_kernel<1, false><<<blocks_for(n, 256), 256, 0, st>>>(a, r, b, nullptr);
         dt_minmax_kernel<2, true><<<blocks_for(n, 256), 256, 0, st>>>(b, r, nullptr, out);
