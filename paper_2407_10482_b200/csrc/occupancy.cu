@@ -147,13 +147,17 @@ __device__ __forceinline__ int cheb_sep(int i, int u, int gi, int gu) {
     return (u - gi) < mid ? (u - gi) : mid;
 }
 // The column is first staged in shared memory (independent coalesced loads, all
-// in flight at once), so the sequential envelope sweep reads no global memory.
-template <int AXIS, bool FINAL, int NMAX>
+// in flight at once) and the envelope stacks live in shared memory too (IT =
+// u8 indices for r <= 256), so the sequential sweep touches no global or local
+// memory: per CTA r x C x (2 + 2 sizeof(IT)) bytes.
+template <int AXIS, bool FINAL, typename IT>
 __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restrict__ in, int r,
                                                          uint16_t* __restrict__ out,
                                                          uint8_t* __restrict__ out8) {
-    extern __shared__ uint16_t colbuf[];  // [r][blockDim.x]
+    extern __shared__ uint16_t colbuf[];  // [r][C] column, then s [r][C], t [r][C]
     const int C = blockDim.x, tid = threadIdx.x;
+    IT* s = reinterpret_cast<IT*>(colbuf + size_t(r) * C) + tid;
+    IT* t = s + size_t(r) * C;
     const size_t col = blockIdx.x * size_t(C) + tid;
     const bool live = col < size_t(r) * r;
     // AXIS 1 (y): column (x, z), element u at (z * r + u) * r + x
@@ -165,33 +169,42 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
     uint16_t* g = colbuf + tid;
 #pragma unroll 8
     for (int u = 0; u < r; ++u) g[u * C] = in[base + size_t(u) * stride];
-    uint16_t s[NMAX], t[NMAX];  // NMAX >= r: envelope stacks (local memory, L1)
-    int q = 0;
+    // stack entry q at s[q * C] / t[q * C]; the top (sq, tq, gs) is kept in registers
+    int q = 0, sq = 0, tq = 0;
     s[0] = 0;
     t[0] = 0;
-    int gs = g[0];  // g(s[q]), kept in a register
+    int gs = g[0];  // g(s[q])
     for (int u = 1; u < r; ++u) {
         const int gu = g[u * C];
-        while (q >= 0 && cheb_f(t[q], s[q], gs) > cheb_f(t[q], u, gu)) {
+        while (q >= 0 && cheb_f(tq, sq, gs) > cheb_f(tq, u, gu)) {
             --q;
-            if (q >= 0) gs = g[s[q] * C];
+            if (q >= 0) {
+                sq = s[q * C];
+                tq = t[q * C];
+                gs = g[sq * C];
+            }
         }
         if (q < 0) {
             q = 0;
-            s[0] = uint16_t(u);
+            sq = u;
+            tq = 0;
+            s[0] = IT(u);
+            t[0] = 0;
             gs = gu;
         } else {
-            const int w = 1 + cheb_sep(s[q], u, gs, gu);
+            const int w = 1 + cheb_sep(sq, u, gs, gu);
             if (w < r) {
                 ++q;
-                s[q] = uint16_t(u);
-                t[q] = uint16_t(w);
+                sq = u;
+                tq = w;
+                s[q * C] = IT(u);
+                t[q * C] = IT(w);
                 gs = gu;
             }
         }
     }
     for (int u = r - 1; u >= 0; --u) {
-        const int h = cheb_f(u, s[q], gs);
+        const int h = cheb_f(u, sq, gs);
         const size_t i = base + size_t(u) * stride;
         if (FINAL) {
             const int gg = h == 0 ? 0 : h - 1;  // occupancy.hpp:188-192
@@ -199,9 +212,11 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
         } else {
             out[i] = uint16_t(h < int(kInf) ? h : int(kInf));
         }
-        if (u == t[q] && q > 0) {
+        if (u == tq && q > 0) {
             --q;
-            gs = g[s[q] * C];
+            sq = s[q * C];
+            tq = t[q * C];
+            gs = g[sq * C];
         }
     }
 }
@@ -251,14 +266,26 @@ void launch_distance_grid(const uint32_t* occ, int r, uint16_t* a, uint16_t* b, 
     dt_minmax_kernel<1, false><<<blocks_for(n, 256), 256, 0, st>>>(a, r, b, nullptr);
     dt_minmax_kernel<2, true><<<blocks_for(n, 256), 256, 0, st>>>(b, r, nullptr, out);
 #else
-    if (r <= 256) {  // 64 columns x r x 2 B of staging per CTA (<= 32 KB)
-        const size_t sm = size_t(r) * 64 * 2;
-        dt_envelope_kernel<1, false, 256><<<blocks_for(rows, 64), 64, sm, st>>>(a, r, b, nullptr);
-        dt_envelope_kernel<2, true, 256><<<blocks_for(rows, 64), 64, sm, st>>>(b, r, nullptr, out);
-    } else if (r <= 1024) {  // 16 columns per CTA (<= 32 KB)
-        const size_t sm = size_t(r) * 16 * 2;
-        dt_envelope_kernel<1, false, 1024><<<blocks_for(rows, 16), 16, sm, st>>>(a, r, b, nullptr);
-        dt_envelope_kernel<2, true, 1024><<<blocks_for(rows, 16), 16, sm, st>>>(b, r, nullptr, out);
+    static PerDeviceInt attrs;  // opt in to > 48 KB of dynamic shared memory, once per device
+    attrs.get([](int) {
+        cudaFuncSetAttribute(dt_envelope_kernel<1, false, uint8_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 64 * 4);
+        cudaFuncSetAttribute(dt_envelope_kernel<2, true, uint8_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 64 * 4);
+        cudaFuncSetAttribute(dt_envelope_kernel<1, false, uint16_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16 * 6);
+        cudaFuncSetAttribute(dt_envelope_kernel<2, true, uint16_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16 * 6);
+        return 1;
+    });
+    if (r <= 256) {  // 64 columns per CTA, u8 stack indices: r x 64 x 4 B (<= 64 KB)
+        const size_t sm = size_t(r) * 64 * 4;
+        dt_envelope_kernel<1, false, uint8_t><<<blocks_for(rows, 64), 64, sm, st>>>(a, r, b, nullptr);
+        dt_envelope_kernel<2, true, uint8_t><<<blocks_for(rows, 64), 64, sm, st>>>(b, r, nullptr, out);
+    } else if (r <= 1024) {  // 16 columns per CTA, u16 stack indices: r x 16 x 6 B (<= 96 KB)
+        const size_t sm = size_t(r) * 16 * 6;
+        dt_envelope_kernel<1, false, uint16_t><<<blocks_for(rows, 16), 16, sm, st>>>(a, r, b, nullptr);
+        dt_envelope_kernel<2, true, uint16_t><<<blocks_for(rows, 16), 16, sm, st>>>(b, r, nullptr, out);
     } else {  // beyond the envelope stacks' size: the outward search
         dt_minmax_kernel<1, false><<<blocks_for(n, 256), 256, 0, st>>>(a, r, b, nullptr);
         dt_minmax_kernel<2, true><<<blocks_for(n, 256), 256, 0, st>>>(b, r, nullptr, out);
