@@ -44,6 +44,21 @@ bool fp16_exact(float v) {
 
 float host_sigmoid(float x) { return 1.0f / (1.0f + std::exp(-x)); }  // nn.hpp:91-94 (glibc expf)
 
+// Per-call scratch (renders, the distance transform) comes from the current
+// device's stream-ordered pool; keep its memory mapped across synchronisations
+// instead of trimming to zero (once per device).
+void keep_pool_mapped() {
+    static PerDeviceInt done;
+    done.get([](int dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~uint64_t(0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        return 1;
+    });
+}
+
 }  // namespace
 
 namespace ngprt_host {
@@ -238,15 +253,7 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
         return fail(NGPRT_ENODEV, std::string("this build targets sm_100a (B200); device is ") +
                                       prop.name);
     NG_CUDA(cudaSetDevice(device));
-    {
-        // Per-render scratch comes from the device's stream-ordered pool; keep its
-        // memory mapped across synchronisations instead of trimming to zero.
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t keep = ~uint64_t(0);
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-    }
+    keep_pool_mapped();
 
     // --- storage decision: fp16 only when lossless ---
     int storage = d->storage;
@@ -899,6 +906,7 @@ ngprt_status ngprt_build_distance_grid(const uint64_t* occ, uint32_t res, uint8_
     if (res > 32768) return fail(NGPRT_EINVAL, "resolution too large");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t n = size_t(res) * res * res;
+    keep_pool_mapped();
     uint16_t *a, *b;
     NG_CUDA(cudaMallocAsync(&a, n * 2, st));
     NG_CUDA(cudaMallocAsync(&b, n * 2, st));

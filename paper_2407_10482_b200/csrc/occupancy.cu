@@ -154,7 +154,7 @@ template <int AXIS, bool FINAL, typename IT>
 __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restrict__ in, int r,
                                                          uint16_t* __restrict__ out,
                                                          uint8_t* __restrict__ out8) {
-    extern __shared__ uint16_t colbuf[];  // [r][C] column, then s [r][C], t [r][C]
+    extern __shared__ __align__(16) uint16_t colbuf[];  // [r][C] column, then s [r][C], t [r][C]
     const int C = blockDim.x, tid = threadIdx.x;
     IT* s = reinterpret_cast<IT*>(colbuf + size_t(r) * C) + tid;
     IT* t = s + size_t(r) * C;
@@ -165,10 +165,25 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
     const size_t x = col % size_t(r), o = col / size_t(r);
     const size_t base = AXIS == 1 ? o * size_t(r) * r + x : o * size_t(r) + x;
     const size_t stride = AXIS == 1 ? size_t(r) : size_t(r) * r;
-    if (!live) return;  // no block-wide synchronisation below: each thread owns its column
     uint16_t* g = colbuf + tid;
+    if (r % C == 0 && C % 8 == 0) {
+        // the CTA's C columns are C consecutive x of one row: stage the r segments of
+        // C u16 cooperatively with 16 B loads (C / 8 threads per segment)
+        const size_t x0 = (blockIdx.x * size_t(C)) % size_t(r), o0 = (blockIdx.x * size_t(C)) / size_t(r);
+        const size_t b0 = AXIS == 1 ? o0 * size_t(r) * r + x0 : o0 * size_t(r) + x0;
+        const int per = C / 8, segs_per_pass = blockDim.x / per;
+#pragma unroll 4
+        for (int u = tid / per; u < r; u += segs_per_pass) {
+            const uint4 v = *reinterpret_cast<const uint4*>(in + b0 + size_t(u) * stride + (tid % per) * 8);
+            *reinterpret_cast<uint4*>(colbuf + size_t(u) * C + (tid % per) * 8) = v;
+        }
+        __syncthreads();
+        if (!live) return;
+    } else {
+        if (!live) return;  // each thread stages and sweeps its own column
 #pragma unroll 8
-    for (int u = 0; u < r; ++u) g[u * C] = in[base + size_t(u) * stride];
+        for (int u = 0; u < r; ++u) g[u * C] = in[base + size_t(u) * stride];
+    }
     // stack entry q at s[q * C] / t[q * C]; the top (sq, tq, gs) is kept in registers
     int q = 0, sq = 0, tq = 0;
     s[0] = 0;
