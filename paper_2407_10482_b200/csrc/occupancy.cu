@@ -2,8 +2,9 @@
 // scene layout kernels.
 //
 // K3 restates BitGrid::downsampled2 (occupancy.hpp:40-51) / build_pyramid
-// (:114-119): one thread per parent voxel ORs its 8 children; a warp ballot
-// assembles 32 parent bits into one little-endian u32 of the u64 word layout.
+// (:114-119): one thread per output u32 (32 parents along x) ORs the 4 child
+// rows' 64-bit words and compacts the bit pairs; levels whose rows are not a
+// multiple of 32 voxels take one thread per parent voxel and a warp ballot.
 //
 // K4 computes the same grid as build_distance_grid (:136-194) — exact
 // Chebyshev distance, G = min(255, max(0, D-1)), all-empty -> 255 — but as a
@@ -38,6 +39,36 @@ __global__ void pyramid_kernel(const uint32_t* __restrict__ src, int rs, uint32_
     }
     const unsigned m = __ballot_sync(0xffffffffu, v);
     if ((threadIdx.x & 31) == 0 && i < n) dst[i >> 5] = m;
+}
+
+// Word-level K3 (parent rows a multiple of 32 voxels): one thread per output u32,
+// i.e. 32 parents along x. Their children are 64 bits (two u32) in each of the 4
+// child rows (y, z parity); OR the rows, OR each bit pair, and compact the even
+// bits: 8 loads per 32 parents instead of 8 per parent.
+__device__ __forceinline__ uint32_t even_bits(uint64_t v) {  // bit 2j -> bit j
+    v &= 0x5555555555555555ull;
+    v = (v | (v >> 1)) & 0x3333333333333333ull;
+    v = (v | (v >> 2)) & 0x0f0f0f0f0f0f0f0full;
+    v = (v | (v >> 4)) & 0x00ff00ff00ff00ffull;
+    v = (v | (v >> 8)) & 0x0000ffff0000ffffull;
+    v = (v | (v >> 16)) & 0x00000000ffffffffull;
+    return uint32_t(v);
+}
+__global__ void pyramid_word_kernel(const uint32_t* __restrict__ src, int rs,
+                                    uint32_t* __restrict__ dst, int ro) {
+    const size_t nw = size_t(ro) * ro * ro / 32;
+    const size_t w = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (w >= nw) return;
+    const size_t p0 = w * 32;  // first parent voxel of this word
+    const int xw = int(p0 % ro), y = int((p0 / ro) % ro), z = int(p0 / (size_t(ro) * ro));
+    uint64_t v = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const size_t bit = size_t(2 * xw) + size_t(rs) * (size_t(2 * y + (c & 1)) + size_t(rs) * size_t(2 * z + (c >> 1)));
+        const uint2 pr = *reinterpret_cast<const uint2*>(src + (bit >> 5));  // 64-bit aligned: rs % 64 == 0
+        v |= uint64_t(pr.x) | (uint64_t(pr.y) << 32);
+    }
+    dst[w] = even_bits(v | (v >> 1));
 }
 
 // Pass X: per row (y, z), distance to the nearest occupied voxel along x. One
@@ -266,7 +297,10 @@ unsigned blocks_for(size_t n, unsigned bs) { return unsigned((n + bs - 1) / bs);
 void launch_pyramid_level(const uint32_t* src, int src_res, uint32_t* dst, cudaStream_t st) {
     const int ro = src_res / 2;
     const size_t n = size_t(ro) * ro * ro;
-    pyramid_kernel<<<blocks_for(n, 256), 256, 0, st>>>(src, src_res, dst, ro);
+    if (ro % 32 == 0)  // every output word is 32 parents of one row
+        pyramid_word_kernel<<<blocks_for(n / 32, 256), 256, 0, st>>>(src, src_res, dst, ro);
+    else
+        pyramid_kernel<<<blocks_for(n, 256), 256, 0, st>>>(src, src_res, dst, ro);
 }
 
 void launch_distance_grid(const uint32_t* occ, int r, uint16_t* a, uint16_t* b, uint8_t* out,

@@ -213,3 +213,43 @@ def test_bench_tile_sharding_mode_two_ranks_on_one_gpu():
     d = lines[0]
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["gpu_launches"] == 3 * 3 + 3  # rank 0: K0/K1/K2 + assemble per step
+
+
+def _compact_index_model(W, H, world, tile):
+    """Python model of the compact shard layout (include/ngprt_cuda.h,
+    ngprt_render_opts.shard_*): rank -> list of (slot, x, y) for real pixels."""
+    tx = (W + tile - 1) // tile
+    n = tx * ((H + tile - 1) // tile)
+    local = (n + world - 1) // world
+    out = {r: [] for r in range(world)}
+    for r in range(world):
+        for j in range(local):
+            T = r + j * world
+            if T >= n:
+                continue
+            for ly in range(tile):
+                for lx in range(tile):
+                    x, y = (T % tx) * tile + lx, (T // tx) * tile + ly
+                    if x < W and y < H:
+                        out[r].append((j * tile * tile + ly * tile + lx, x, y))
+    return out, local * tile * tile
+
+
+@pytest.mark.parametrize("W,H,world,tile", [(37, 23, 2, 8), (70, 44, 3, 16), (64, 64, 4, 32),
+                                            (250, 130, 8, 32), (40, 8, 7, 8)])
+def test_compact_shard_layout_covers_every_pixel_once(ng, W, H, world, tile):
+    """The compact layout: every pixel of the window lands in exactly one slot of
+    one rank, the per-rank size equals ngprt_shard_pixels (C ABI, no GPU needed),
+    and the rank's tiles are tile_windows' tiles in the same order."""
+    model, per_rank = _compact_index_model(W, H, world, tile)
+    assert per_rank == int(ng.lib().ngprt_shard_pixels(W, H, world, tile))
+    seen = torch.zeros(H, W, dtype=torch.int32)
+    for r in range(world):
+        slots = [s for s, _, _ in model[r]]
+        assert len(set(slots)) == len(slots) and max(slots, default=0) < per_rank
+        for _, x, y in model[r]:
+            seen[y, x] += 1
+        wins = mg.tile_windows(W, H, tile, r, world)
+        firsts = [(x, y) for s, x, y in model[r] if s % (tile * tile) == 0]
+        assert firsts == [(x0, y0) for (x0, y0, _, _) in wins]
+    assert bool((seen == 1).all())
