@@ -63,7 +63,11 @@ typedef enum {
 
 /* How feature rows are stored in HBM. AUTO picks fp16 when every coarse row
  * and fine-table value survives an f32->f16->f32 round trip (lossless, so the
- * render stays bit-exact), else f32. */
+ * render stays bit-exact), else f32. F16 forced on values that are not
+ * fp16-exact is an opt-in LOSSY mode (round to nearest): on the f32 config-3
+ * scene it renders 1.38x faster than F32 with RGB max-abs 4.4e-4 (<= 1e-3,
+ * PSNR 93 dB), and ~0.1 % of rays change their counters (early stop moves);
+ * tests/test_gpu_parity.py::test_forced_fp16_storage_is_within_tolerance. */
 typedef enum { NGPRT_STORAGE_AUTO = 0, NGPRT_STORAGE_F32 = 1, NGPRT_STORAGE_F16 = 2 } ngprt_storage;
 
 /* Deferred MLP (shade, volume.hpp:118-137) implementation.

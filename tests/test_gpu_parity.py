@@ -417,3 +417,20 @@ def test_render_without_counters_is_identical(ng, torch, mlp):
         torch.cuda.synchronize()
         rgb = rgb[0].cpu().numpy()
         assert np.array_equal(rgb.view(np.uint32), rgb_s.view(np.uint32)), case["name"]
+
+
+def test_forced_fp16_storage_is_within_tolerance(ng, torch):
+    """The opt-in lossy mode: an f32 scene (values not fp16-representable) stored
+    as fp16 anyway (storage = NGPRT_STORAGE_F16) renders within the north_star
+    RGB tolerance of the compiled reference (max-abs <= 1e-3, PSNR >= 60 dB) on a
+    full 1080p frame of config 3; the counters may differ where early stop moves."""
+    scene = ng.SynthScene(**dict(ng.CONFIGS["c3_1080p_f32"]))
+    dev = ng.Scene(scene, storage=ng._abi.STORAGE_F16)
+    assert dev.info().storage == 2
+    cam = ng.cameras(64, 1920, 1080)[6]
+    rgb = ng.render(dev, [cam], ng.Opts())
+    torch.cuda.synchronize()
+    want_rgb, want_st = ref_scene(scene.desc_ptr).render(cam, ng.Opts(mlp="exact").to_c())
+    got = rgb[0].cpu().numpy()
+    assert np.abs(got - want_rgb).max() <= RGB_TOL
+    assert psnr(got, want_rgb) >= PSNR_MIN
