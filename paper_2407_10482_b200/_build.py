@@ -56,8 +56,7 @@ def _run(cmd):
 
 def build(verbose: bool = False, ptxas_verbose: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
-    objs = []
-    changed = False
+    objs, cmds = [], []
     for src, extra in UNITS:
         s = CSRC / src
         o = OBJ / (src + ".o")
@@ -72,10 +71,14 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> Path:
                     cmd.insert(1, "-Xptxas=-v")
             if verbose:
                 print(" ".join(cmd))
-            r = _run(cmd)
+            cmds.append(cmd)
+    changed = bool(cmds)
+    # translation units compile in parallel (march.cu, the longest, goes first)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for r in list(ex.map(_run, cmds)):
             if ptxas_verbose:
                 sys.stderr.write(r.stderr)
-            changed = True
     if changed or not LIB.exists():
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread", "-ldl", "-lrt"]
         if verbose:

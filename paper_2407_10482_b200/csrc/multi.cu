@@ -223,6 +223,7 @@ ngprt_status ngprt_shard_assemble(const float* shards, uint32_t world, uint32_t 
 
 ngprt_status ngprt_multi_create(const ngprt_scene_desc* desc, const int* devices, int n_dev,
                                 ngprt_multi** out) {
+    const ngprt_dev::DeviceRestore keep;
     if (!desc || !devices || n_dev < 1 || !out) return fail(NGPRT_EINVAL, "ngprt_multi_create: bad argument");
     *out = nullptr;
     auto* m = new ngprt_multi;
@@ -267,7 +268,10 @@ ngprt_status ngprt_multi_create(const ngprt_scene_desc* desc, const int* devices
     return NGPRT_OK;
 }
 
-void ngprt_multi_destroy(ngprt_multi* m) { delete m; }
+void ngprt_multi_destroy(ngprt_multi* m) {
+    const ngprt_dev::DeviceRestore keep;
+    delete m;
+}
 
 int ngprt_multi_uses_nccl(const ngprt_multi* m) { return m && m->use_nccl ? 1 : 0; }
 
@@ -278,6 +282,7 @@ const ngprt_scene* ngprt_multi_scene(const ngprt_multi* m, int i) {
 ngprt_status ngprt_multi_render_tiles(ngprt_multi* m, const ngprt_camera* cams, int n_cams,
                                       const ngprt_render_opts* opts, uint32_t tile, float* rgb0,
                                       ngprt_ray_stats* stats0, void* stream0) {
+    const ngprt_dev::DeviceRestore keep;
     if (!m || !cams || n_cams <= 0 || !opts || !rgb0)
         return fail(NGPRT_EINVAL, "ngprt_multi_render_tiles: bad argument");
     tile = tile ? tile : 32u;
@@ -352,6 +357,7 @@ ngprt_status ngprt_multi_render_tiles(ngprt_multi* m, const ngprt_camera* cams, 
 ngprt_status ngprt_multi_render_cameras(ngprt_multi* m, const ngprt_camera* cams, int n_cams,
                                         const ngprt_render_opts* opts, float* rgb0,
                                         ngprt_ray_stats* stats0, void* stream0) {
+    const ngprt_dev::DeviceRestore keep;
     if (!m || !cams || n_cams <= 0 || !opts || !rgb0)
         return fail(NGPRT_EINVAL, "ngprt_multi_render_cameras: bad argument");
     if (opts->shard_world) return fail(NGPRT_EINVAL, "ngprt_multi_render_cameras: opts are sharded");

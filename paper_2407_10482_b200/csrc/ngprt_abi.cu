@@ -166,6 +166,7 @@ int ngprt_abi_version(void) { return NGPRT_ABI_VERSION; }
 const char* ngprt_last_error(void) { return g_err.c_str(); }
 
 ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_scene** out) {
+    const DeviceRestore keep;
     if (!d || !out) return fail(NGPRT_EINVAL, "ngprt_scene_create: null argument");
     *out = nullptr;
     // --- validation (mirrors the reference's invariants) ---
@@ -681,12 +682,14 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
 ngprt_status ngprt_render(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
                           const ngprt_render_opts* o, float* rgb_dev, ngprt_ray_stats* stats_dev,
                           void* stream) {
+    const DeviceRestore keep;
     return render_impl(s, cams, n_cams, o, rgb_dev, stats_dev, static_cast<cudaStream_t>(stream));
 }
 
 ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
                                const ngprt_render_opts* o, float* rgb_host,
                                ngprt_ray_stats* stats_host) {
+    const DeviceRestore keep;
     if (!s || !cams || !o || !rgb_host) return fail(NGPRT_EINVAL, "ngprt_render_host: null argument");
     if (n_cams <= 0) return fail(NGPRT_EINVAL, "ngprt_render_host: n_cams must be > 0");
     NG_CUDA(cudaSetDevice(s->device));
@@ -793,6 +796,7 @@ ngprt_status ngprt_render_host(const ngprt_scene* s, const ngprt_camera* cams, i
 ngprt_status ngprt_render_host_async(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
                                      const ngprt_render_opts* o, float* rgb_host,
                                      ngprt_ray_stats* stats_host) {
+    const DeviceRestore keep;
     if (!s || !cams || !o || !rgb_host)
         return fail(NGPRT_EINVAL, "ngprt_render_host_async: null argument");
     if (n_cams <= 0) return fail(NGPRT_EINVAL, "ngprt_render_host_async: n_cams must be > 0");
@@ -844,6 +848,7 @@ ngprt_status ngprt_render_host_async(const ngprt_scene* s, const ngprt_camera* c
 }
 
 ngprt_status ngprt_render_host_wait(const ngprt_scene* s) {
+    const DeviceRestore keep;
     if (!s) return fail(NGPRT_EINVAL, "ngprt_render_host_wait: null scene");
     std::lock_guard<std::mutex> lock(s->async.mu);
     auto& ac = s->async;

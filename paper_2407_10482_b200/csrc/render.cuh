@@ -17,6 +17,23 @@ inline int current_device() {
     cudaGetDevice(&d);
     return (d >= 0 && d < kMaxDevices) ? d : 0;
 }
+// The C-ABI entry points switch to their scene's device; the caller's current
+// device is restored on return (a host thread may interleave calls on several
+// devices, and frameworks such as torch keep their own notion of it).
+struct DeviceRestore {
+    int prev = -1;
+    DeviceRestore() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            cudaGetLastError();
+        }
+    }
+    ~DeviceRestore() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceRestore(const DeviceRestore&) = delete;
+    DeviceRestore& operator=(const DeviceRestore&) = delete;
+};
 struct PerDeviceInt {
     std::once_flag once[kMaxDevices];
     int value[kMaxDevices] = {};
