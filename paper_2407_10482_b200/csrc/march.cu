@@ -975,6 +975,55 @@ __device__ __forceinline__ uint32_t probe_index(uint32_t x, uint32_t y, uint32_t
 #ifndef NGPRT_EXIT_SEL
 #define NGPRT_EXIT_SEL 1
 #endif
+// Park-time L1 prefetch (NGPRT_PARK_PREFETCH bits: 1 coarse rows, 2 fine level 0,
+// 4 fine level 1): a lane that reaches an occupied point requests its sample's
+// rows into L1 with register-free prefetches, so the warp's later decode (when
+// enough lanes have parked) hits L1 instead of waiting on L2.
+#ifndef NGPRT_PARK_PREFETCH
+#define NGPRT_PARK_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void park_prefetch(const DevScene& sc, const float x[3]) {
+#if NGPRT_PARK_PREFETCH
+    if (!sc.fast_decode) return;
+    const bool f16 = sc.storage == NGPRT_STORAGE_F16;
+    if (NGPRT_PARK_PREFETCH & 1) {
+        int cb[3];
+        float cf[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.coarse_h, sc.L_C, cb[a], cf[a]);
+        const uint32_t r1 = uint32_t(sc.L_C) + 1;
+        const uint32_t key0 = uint32_t(cb[0]) + r1 * (uint32_t(cb[1]) + r1 * uint32_t(cb[2]));
+        const char* base = static_cast<const char*>(sc.coarse);
+        const size_t row_bytes = f16 ? 32 : 64;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            prefetch_l1(base + size_t(key0 + (k & 1) + ((k >> 1) & 1) * r1 + (k >> 2) * r1 * r1) * row_bytes);
+    }
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+        if (!((NGPRT_PARK_PREFETCH >> (1 + l)) & 1) || l >= sc.L) continue;
+        int b[3];
+        float f[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) stencil_axis(x[a], sc.fine_h[l], sc.fine_res[l], b[a], f[a]);
+        const uint32_t mask = sc.fine_mask[l];
+        const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
+        const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
+        const char* table = static_cast<const char*>(sc.fine[l]);
+        const size_t row_bytes = f16 ? 16 : 32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            prefetch_l1(table + size_t((uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask) * row_bytes);
+    }
+#else
+    (void)sc;
+    (void)x;
+#endif
+}
+
 // One marching point (march, occupancy.hpp:310-324): probe (:218-231) via the
 // per-level-1 probe code; occupied -> park for decode; empty -> next_step (:261-276).
 // Returns false when the ray left the clip interval.
@@ -1006,6 +1055,7 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     if ((code >> child) & (code >> 15) & 1u) {
         if constexpr (STATS) ++s.n_occ;
         s.pending = true;
+        park_prefetch(sc, xc);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             if constexpr (kLaneSmem) lane_row(scr, lb, a) = xc[a];
