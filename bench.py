@@ -164,38 +164,29 @@ class Clocks:
                 "samples": len(self.lines)}
 
 
-def cpu_sample(scene_synth, cam, W, H, seconds, kind_pref="reference"):
-    """Bounded CPU-baseline sample: horizontal bands of the same camera rendered by
-    oracle/_ref (the reference itself) when present, else the C restatement."""
+def cpu_sample(scene_synth, cams, W, H, seconds, kind_pref="reference"):
+    """Bounded CPU-baseline sample: FULL frames of the timed cameras (the same
+    frames the GPU renders) by oracle/_ref (the reference itself) when present,
+    else the C restatement, with every host thread, until `seconds` of work; plus
+    the one-thread rate on a 4-row band (1 thread and nproc)."""
     sys.path.insert(0, str(ROOT / "tests"))
     from checkers import REF_SO, CpuScene
     import paper_2407_10482_b200 as ng
     kind = "reference" if (kind_pref == "reference" and REF_SO.exists()) else "port"
     cs = CpuScene(scene_synth.desc_ptr, "ref" if kind == "reference" else "oracle")
     threads = os.cpu_count() or 1
-    # one host thread on a small band first (SURVEY.md §8(d): 1 thread and nproc)
     r1 = 4
     t = time.perf_counter()
-    cs.render(cam, ng.Opts(window=(0, H // 2 - r1 // 2, W, r1)).to_c(), nthreads=1)
+    cs.render(cams[0], ng.Opts(window=(0, H // 2 - r1 // 2, W, r1)).to_c(), nthreads=1)
     one_thread_mrays = W * r1 / (time.perf_counter() - t) / 1e6
-    rows = 8
-    y0 = H // 2 - rows // 2
-    t = time.perf_counter()
-    cs.render(cam, ng.Opts(window=(0, y0, W, rows)).to_c(), nthreads=threads)
-    dt = time.perf_counter() - t
-    rows = int(max(8, min(H, rows * seconds / max(dt, 1e-3))))
-    # the sample: 8 equal bands spread evenly over the frame height (ray cost
-    # varies strongly with the row), each rendered with every host thread
-    nb = 8 if rows >= 8 * 16 else 1
-    bh = max(1, rows // nb)
-    t = time.perf_counter()
-    for k in range(nb):
-        y0 = int((k + 0.5) / nb * (H - bh))
-        cs.render(cam, ng.Opts(window=(0, y0, W, bh)).to_c(), nthreads=threads)
-    dt = time.perf_counter() - t
+    dt, frames = 0.0, 0
+    while frames < len(cams) and (frames == 0 or dt < seconds):
+        t = time.perf_counter()
+        cs.render(cams[frames], ng.Opts().to_c(), nthreads=threads)
+        dt += time.perf_counter() - t
+        frames += 1
     cs.close()
-    rows = nb * bh
-    rays = W * rows
+    rays = W * H * frames
     model = ""
     try:
         for l in open("/proc/cpuinfo"):
@@ -205,10 +196,10 @@ def cpu_sample(scene_synth, cam, W, H, seconds, kind_pref="reference"):
     except OSError:
         pass
     return {"kind": kind, "cores": threads, "rays": rays, "seconds": dt,
-            "mrays_per_s": rays / dt / 1e6, "fps": rays / dt / (W * H),
+            "mrays_per_s": rays / dt / 1e6, "fps": frames / dt,
             "one_thread_mrays_per_s": one_thread_mrays, "cpu_model": model,
-            "sample": f"{W}x{rows} rows of camera 0 in {nb} bands spread over the frame, "
-                      f"{threads} threads"}
+            "sample": f"{frames} full {W}x{H} frame(s) of the timed cameras, {threads} threads "
+                      f"(one-thread rate from a {W}x{r1} band)"}
 
 
 def run_reference(args):
@@ -652,7 +643,8 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_sample(synth, cams_of(0)[0], W, H, args.cpu_seconds)
+            cb = cpu_sample(synth, [cams_of(args.warmup + i)[0] for i in range(args.steps)], W, H,
+                            args.cpu_seconds)
             line["cpu_baseline"] = {"value": cb["fps"], "unit": UNIT, "cores": cb["cores"],
                                     "kind": cb["kind"], "sample": cb["sample"],
                                     "mrays_per_s": cb["mrays_per_s"],
