@@ -103,19 +103,24 @@ def algorithmic_bytes(stats, L, b_c=2, b_f=2):
     return float((s[:, 1] * per_sample + 4 * s[:, 2] + 1 * s[:, 3]).sum() + 12 * s.shape[0])
 
 
-def binding_ceiling(l2_bytes, dram_bytes, k1_ms, ceilings):
-    """Name the resource that binds K1: its measured L2 sector traffic against the
-    L2-resident random 32 B-gather peak measured on this B200 (the access pattern
-    K1 has), and its DRAM traffic against the HBM copy peak."""
-    if not l2_bytes or not ceilings or "l2_gather32_gbs" not in ceilings:
+def binding_ceiling(tj, k1_ms, ceilings):
+    """Name what binds K1, from the ncu capture of the same build (tj, one K1
+    launch) and this run's K1 time: the gather traffic its L1s request from L2
+    (lts__t_sectors_srcunit_tex) against the L2-resident random 32 B-gather rate
+    measured on this B200 and against the L2 slices' own sector throughput, and
+    its DRAM traffic against the HBM copy peak."""
+    if not tj or not tj.get("l2_read_bytes_per_launch"):
         return None
-    l2 = l2_bytes / (k1_ms / 1e3) / 1e9
-    g = ceilings["l2_gather32_gbs"]["peak_gbs"]
-    out = {"ceiling": "L2 random 32 B-sector gather (L2-resident tables)", "peak_gbs": g,
-           "achieved_gbs": l2, "frac": l2 / g}
-    if dram_bytes:
+    l2 = tj["l2_read_bytes_per_launch"] / (k1_ms / 1e3) / 1e9
+    out = {"l2_read_gbs": l2, "l2_slice_util_pct_ncu": tj.get("l2_slice_util_pct")}
+    if ceilings and "l2_gather32_gbs" in ceilings:
+        g = ceilings["l2_gather32_gbs"]["peak_gbs"]
+        out.update(gather32_peak_gbs=g, gather32_frac=l2 / g)
+    if tj.get("dram_bytes_per_launch"):
         peak, _ = load_peaks()
-        out["dram_frac_of_hbm_peak"] = dram_bytes / (k1_ms / 1e3) / 1e9 / peak
+        out["dram_frac_of_hbm_peak"] = tj["dram_bytes_per_launch"] / (k1_ms / 1e3) / 1e9 / peak
+    out["verdict"] = ("gather-latency bound: neither the L2 slices nor DRAM are near their "
+                      "throughput (see DESIGN.md §4)")
     return out
 
 
@@ -557,6 +562,7 @@ def run_ours(args):
         k1_avg = sum(k1_ms) / len(k1_ms)
         achieved = (bytes_k1 / args.steps) / (k1_avg / 1e3) / 1e9
         traffic = l2_traffic = None
+        tj = {}
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
             tj = json.loads(tp.read_text()).get(args.config, {})
@@ -619,7 +625,7 @@ def run_ours(args):
                          # this run's K1 event time, and the ceiling that binds
                          "l2_gbs": (l2_traffic / (k1_avg / 1e3) / 1e9) if l2_traffic else None,
                          "dram_gbs": (traffic / (k1_avg / 1e3) / 1e9) if traffic else None,
-                         "binding_ceiling": binding_ceiling(l2_traffic, traffic, k1_avg, ceilings)},
+                         "binding_ceiling": binding_ceiling(tj, k1_avg, ceilings)},
             "k2_tensor": {"kernel": "shade_tc_kernel (K2)" if args.mlp == "tensor" else "shade_exact_kernel",
                           "shaded_rays": int(shaded), "flop_per_launch": k2_flop,
                           "achieved_tflops": k2_flop / (k2_avg * 1e-3) / 1e12,

@@ -91,7 +91,7 @@ def main():
     lines = [f"# ncu summary `{tag}`", "",
              f"Source: `{rep.name}` (`ncu --set full --clock-control none`, cold L2 per replay) and "
              f"`{launches.name}` (`--metrics gpu__time_duration.sum`, every launch).", ""]
-    traffic = l2 = None
+    traffic = l2 = l2_read = l2_util = None
     for row in data:
         name = row[h.index("Kernel Name")]
         short = name.split("(")[0].replace("void ", "").replace("ngprt_dev::<unnamed>::", "").replace("unnamed>::", "")
@@ -113,6 +113,14 @@ def main():
                 l2 = float(row[k]) * UNIT_SCALE.get(units[k], 1)
             elif "lts__t_sectors.sum" in h:  # 32 B sectors
                 l2 = float(row[h.index("lts__t_sectors.sum")]) * 32.0
+            # the gather traffic proper: sectors the SMs' L1s request from L2, and
+            # how busy the L2 slices are with them
+            l2_read = l2_util = None
+            if "lts__t_sectors_srcunit_tex.sum" in h:
+                l2_read = float(row[h.index("lts__t_sectors_srcunit_tex.sum")]) * 32.0
+            m = "lts__t_sectors_srcunit_tex.avg.pct_of_peak_sustained_elapsed"
+            if m in h:
+                l2_util = float(row[h.index(m)])
         st = stalls(rep, short.split("<")[0].split("::")[-1])
         if st:
             lines.append("")
@@ -130,6 +138,7 @@ def main():
         tp = HERE / "ncu_traffic.json"
         d = json.loads(tp.read_text()) if tp.exists() else {}
         d[config] = {"dram_bytes_per_launch": traffic, "l2_bytes_per_launch": l2,
+                     "l2_read_bytes_per_launch": l2_read, "l2_slice_util_pct": l2_util,
                      "source": f"{rep.name} ({tag})", "kernel": "march_kernel (K1)"}
         tp.write_text(json.dumps(d, indent=1) + "\n")
     print((HERE / f"{tag}_kernels.md").read_text())
