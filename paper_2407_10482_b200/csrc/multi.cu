@@ -283,6 +283,7 @@ ngprt_status ngprt_multi_render_tiles(ngprt_multi* m, const ngprt_camera* cams, 
                                       const ngprt_render_opts* opts, uint32_t tile, float* rgb0,
                                       ngprt_ray_stats* stats0, void* stream0) {
     const ngprt_dev::DeviceRestore keep;
+    const ngprt_dev::NvtxRange range("ngprt_multi_render_tiles");
     if (!m || !cams || n_cams <= 0 || !opts || !rgb0)
         return fail(NGPRT_EINVAL, "ngprt_multi_render_tiles: bad argument");
     tile = tile ? tile : 32u;
@@ -358,6 +359,7 @@ ngprt_status ngprt_multi_render_cameras(ngprt_multi* m, const ngprt_camera* cams
                                         const ngprt_render_opts* opts, float* rgb0,
                                         ngprt_ray_stats* stats0, void* stream0) {
     const ngprt_dev::DeviceRestore keep;
+    const ngprt_dev::NvtxRange range("ngprt_multi_render_cameras");
     if (!m || !cams || n_cams <= 0 || !opts || !rgb0)
         return fail(NGPRT_EINVAL, "ngprt_multi_render_cameras: bad argument");
     if (opts->shard_world) return fail(NGPRT_EINVAL, "ngprt_multi_render_cameras: opts are sharded");

@@ -167,6 +167,7 @@ const char* ngprt_last_error(void) { return g_err.c_str(); }
 
 ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_scene** out) {
     const DeviceRestore keep;
+    const NvtxRange range("ngprt_scene_create");
     if (!d || !out) return fail(NGPRT_EINVAL, "ngprt_scene_create: null argument");
     *out = nullptr;
     // --- validation (mirrors the reference's invariants) ---
@@ -553,6 +554,7 @@ size_t out_pixels_per_cam(const ngprt_render_opts* o, uint32_t W, uint32_t H) {
 ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_cams,
                          const ngprt_render_opts* o, float* rgb, ngprt_ray_stats* stats,
                          cudaStream_t st) {
+    const NvtxRange range(o && o->shard_world ? "ngprt_render (shard)" : "ngprt_render");
     if (!s || !cams || !o || !rgb) return fail(NGPRT_EINVAL, "ngprt_render: null argument");
     if (n_cams <= 0) return fail(NGPRT_EINVAL, "ngprt_render: n_cams must be > 0");
     if (o->keep_level < 0 || o->keep_level > s->ds.L)

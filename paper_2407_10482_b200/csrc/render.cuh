@@ -1,6 +1,8 @@
 // render.cuh — launch-parameter types shared by the render kernels and the C ABI.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <mutex>
 
 #include "device_common.cuh"
@@ -17,6 +19,15 @@ inline int current_device() {
     cudaGetDevice(&d);
     return (d >= 0 && d < kMaxDevices) ? d : 0;
 }
+// NVTX ranges around the C-ABI calls and their phases (header-only NVTX v3: a
+// no-op unless a profiler's injection library is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // The C-ABI entry points switch to their scene's device; the caller's current
 // device is restored on return (a host thread may interleave calls on several
 // devices, and frameworks such as torch keep their own notion of it).
