@@ -331,6 +331,191 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Software-pipelined K2 (default; NGPRT_K2_SEQ=1 selects the kernel above).
+// Layer-1 and layer-2 operands get their own shared-memory planes and their own
+// mbarriers, so a CTA overlaps tile t+1's input staging and layer-1 MMA with
+// tile t's layer-2 MMA and its layer-2 / layer-3 epilogue:
+//   wait L1(t) -> epilogue 1(t) -> issue L2(t) -> stage(t+1) -> issue L1(t+1)
+//   -> wait L2(t) -> epilogue 2(t)
+// Hazards: act1 is rewritten only after L1(t) completed; act2 only after L2(t)
+// completed; TMEM d1 / d2 are rewritten only by MMAs issued after a barrier that
+// follows every thread's tcgen05.ld of them (tcgen05.fence::before_thread_sync).
+// Same arithmetic as the sequential kernel, so the results are identical.
+constexpr int kAct1Bytes = kM * kK1 * 2;  // one plane, K = 32
+constexpr int kAct2Bytes = kM * kH * 2;   // one plane, K = 64
+constexpr int kSmemPipeBytes = kImageBytes + 2 * kAct1Bytes + 2 * kAct2Bytes + 64;
+
+__global__ void __launch_bounds__(kThreads, 3)
+    shade_tc_pipe_kernel(const uint8_t* __restrict__ image, const __grid_constant__ ShadeConsts C,
+                         const RayAcc* __restrict__ acc, float* __restrict__ rgb, size_t n_rays) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* w_img = smem;
+    uint8_t* a1_hi = smem + kImageBytes;
+    uint8_t* a1_lo = a1_hi + kAct1Bytes;
+    uint8_t* a2_hi = a1_lo + kAct1Bytes;
+    uint8_t* a2_lo = a2_hi + kAct2Bytes;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(a2_lo + kAct2Bytes);  // [0] layer 1, [1] layer 2
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < kImageBytes / 16; i += kThreads)
+        reinterpret_cast<uint4*>(w_img)[i] = reinterpret_cast<const uint4*>(image)[i];
+    const uint32_t s_bar1 = uint32_t(__cvta_generic_to_shared(mbar));
+    const uint32_t s_bar2 = uint32_t(__cvta_generic_to_shared(mbar + 1));
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(s_bar1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(s_bar2));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;"
+                     :: "r"(uint32_t(__cvta_generic_to_shared(tmem_slot))));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t d1 = tmem, d2 = tmem + kH;
+    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+    const float* b0 = C.b0;
+    const float* b1 = C.b1;
+    const float* b2 = C.b2;
+    const uint32_t s_w = uint32_t(__cvta_generic_to_shared(w_img));
+    const uint32_t s_a1h = uint32_t(__cvta_generic_to_shared(a1_hi));
+    const uint32_t s_a1l = uint32_t(__cvta_generic_to_shared(a1_lo));
+    const uint32_t s_a2h = uint32_t(__cvta_generic_to_shared(a2_hi));
+    const uint32_t s_a2l = uint32_t(__cvta_generic_to_shared(a2_lo));
+    uint32_t ph1 = 0, ph2 = 0;
+    const size_t n_tiles = (n_rays + kM - 1) / kM;
+
+    // Stage tile `tile`'s layer-1 input rows; returns whether any ray of it is
+    // shaded (then its rows are in act1, fenced for the async proxy).
+    auto stage = [&](size_t tile, const RayAcc& r, bool& shade) -> bool {
+        const size_t ray = tile * kM + tid;
+        shade = ray < n_rays && r.c.w != 0.f && r.a.w < 1.0f;
+        if (!__syncthreads_or(shade)) return false;
+        float x[kK1];
+#pragma unroll
+        for (int i = 0; i < kK1; ++i) x[i] = 0.f;
+        if (shade) {
+            x[0] = r.a.x; x[1] = r.a.y; x[2] = r.a.z;
+            x[3] = r.b.x; x[4] = r.b.y; x[5] = r.b.z; x[6] = r.b.w;
+            sh_encode(r.c.x, r.c.y, r.c.z, x + 7);
+        }
+        store_row_split<kK1>(a1_hi, a1_lo, tid, x);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        return true;
+    };
+    auto issue_l1 = [&]() {
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            issue_layer<kK1>(d1, s_a1h, s_a1l, s_w + kOffW1h, s_w + kOffW1l);
+            mma_commit(s_bar1);
+        }
+    };
+
+    size_t tile = blockIdx.x;
+    if (tile >= n_tiles) goto done;
+    {
+        RayAcc r_cur{}, r_next{};
+        if (tile * kM + tid < n_rays) r_cur = acc[tile * kM + tid];
+        if ((tile + gridDim.x) * kM + tid < n_rays) r_next = acc[(tile + gridDim.x) * kM + tid];
+        bool shade_cur;
+        bool any_cur = stage(tile, r_cur, shade_cur);
+        if (any_cur) issue_l1();
+        while (tile < n_tiles) {
+            const size_t ray = tile * kM + tid;
+            const size_t tn = tile + gridDim.x;
+            if (any_cur) {
+                // ---- layer 1 epilogue -> layer 2 operand, issue layer 2 ----
+                mbar_wait(s_bar1, ph1);
+                ph1 ^= 1u;
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                float h[kH];
+                tmem_ld64(lane_base | d1, h);
+#pragma unroll
+                for (int i = 0; i < kH; i += 2) {
+                    const float2 v = add2(make_float2(h[i], h[i + 1]), make_float2(b0[i], b0[i + 1]));
+                    h[i] = fmaxf(v.x, 0.f);
+                    h[i + 1] = fmaxf(v.y, 0.f);
+                }
+                store_row_split<kH>(a2_hi, a2_lo, tid, h);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncthreads();
+                if (tid == 0) {
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    issue_layer<kH>(d2, s_a2h, s_a2l, s_w + kOffW2h, s_w + kOffW2l);
+                    mma_commit(s_bar2);
+                }
+            }
+            // ---- stage the next tile and issue its layer 1 (overlaps layer 2 of this one) ----
+            RayAcc r_nn{};
+            bool shade_next = false, any_next = false;
+            if (tn < n_tiles) {
+                const size_t nn = (tn + gridDim.x) * kM + tid;
+                if (nn < n_rays) r_nn = acc[nn];
+                any_next = stage(tn, r_next, shade_next);
+                if (any_next) issue_l1();
+            }
+            // ---- layer 2 epilogue + layer 3 (64 -> 3) on CUDA cores ----
+            if (any_cur) {
+                mbar_wait(s_bar2, ph2);
+                ph2 ^= 1u;
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                float h[kH];
+                tmem_ld64(lane_base | d2, h);
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                float2 y01 = make_float2(b2[0], b2[1]);
+                float y2 = b2[2];
+#pragma unroll
+                for (int i = 0; i < kH; i += 2) {
+                    const float2 v = add2(make_float2(h[i], h[i + 1]), make_float2(b1[i], b1[i + 1]));
+                    const float v0 = fmaxf(v.x, 0.f), v1 = fmaxf(v.y, 0.f);
+                    y01 = fma2(make_float2(C.w2p[i][0], C.w2p[i][1]), make_float2(v0, v0), y01);
+                    y2 = fmaf(C.w2c[i], v0, y2);
+                    y01 = fma2(make_float2(C.w2p[i + 1][0], C.w2p[i + 1][1]), make_float2(v1, v1), y01);
+                    y2 = fmaf(C.w2c[i + 1], v1, y2);
+                }
+                const float y[3] = {y01.x, y01.y, y2};
+                if (ray < n_rays) {
+                    float o[3] = {0.f, 0.f, 0.f};
+                    if (shade_cur) {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const float cd = c == 0 ? r_cur.a.x : (c == 1 ? r_cur.a.y : r_cur.a.z);
+                            o[c] = __fdividef(1.0f, 1.0f + __expf(-(cd + y[c])));
+                        }
+                    }
+                    rgb[3 * ray] = o[0];
+                    rgb[3 * ray + 1] = o[1];
+                    rgb[3 * ray + 2] = o[2];
+                }
+            } else if (ray < n_rays) {  // no ray of this tile is shaded: all black
+                rgb[3 * ray] = 0.f;
+                rgb[3 * ray + 1] = 0.f;
+                rgb[3 * ray + 2] = 0.f;
+            }
+            tile = tn;
+            r_cur = r_next;
+            r_next = r_nn;
+            shade_cur = shade_next;
+            any_cur = any_next;
+        }
+    }
+done:
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" :: "r"(tmem));
+    }
+}
+
 }  // namespace
 
 size_t psi_tc_bytes() { return size_t(kImageBytes); }
@@ -372,40 +557,45 @@ void shade_consts_from_psi(const float* psi, ShadeConsts* c) {
     c->b2[3] = 0.f;
 }
 
+#ifndef NGPRT_K2_SEQ
+#define NGPRT_K2_SEQ 0
+#endif
 void launch_shade_tensor(const DevScene&, const void* psi_tc, const ShadeConsts& consts,
                          const RayAcc* acc, float* rgb, size_t n_rays, cudaStream_t st) {
     if (!n_rays) return;
+    auto* kernel = NGPRT_K2_SEQ ? shade_tc_kernel : shade_tc_pipe_kernel;
+    const int smem = NGPRT_K2_SEQ ? kSmemBytes : kSmemPipeBytes;
     static PerDeviceInt grid_of;
-    const int grid = grid_of.get([](int dev) {
-        cudaFuncSetAttribute(shade_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBytes);
-        cudaFuncSetAttribute(shade_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+    const int grid = grid_of.get([&](int dev) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              int(cudaSharedmemCarveoutMaxShared));
         int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const cudaError_t occ_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, shade_tc_kernel, kThreads, kSmemBytes);
+        const cudaError_t occ_err =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, shade_tc_kernel);
+        cudaFuncGetAttributes(&fa, kernel);
         if (std::getenv("NGPRT_VERBOSE"))
             std::fprintf(stderr, "[ngprt] shade_tc occupancy=%d (%s) regs=%d static_smem=%zu max_dyn=%d\n",
                          per_sm, cudaGetErrorString(occ_err), fa.numRegs, fa.sharedSizeBytes,
                          fa.maxDynamicSharedSizeBytes);
-        // 3 x (58.7 KB smem, 128 TMEM columns, 128 x 165 regs) fit one SM; the
-        // occupancy API reports 1 for this kernel, so the grid is sized explicitly
-        // (surplus CTAs would simply run as a later wave). NGPRT_K2_CTAS overrides.
+        // 3 CTAs (their shared memory, 128 TMEM columns and 128 x <= 168 registers
+        // each) fit one SM; the occupancy API reports 1 for these kernels, so the
+        // grid is sized explicitly (surplus CTAs would run as a later wave).
+        // NGPRT_K2_CTAS overrides.
         const char* ov = std::getenv("NGPRT_K2_CTAS");
         per_sm = ov ? std::atoi(ov) : 3;
         per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
         if (std::getenv("NGPRT_VERBOSE"))
             std::fprintf(stderr, "[ngprt] shade_tc: device %d, %d CTAs/SM, grid %d, smem %d B\n", dev,
-                         per_sm, sms * per_sm, kSmemBytes);
+                         per_sm, sms * per_sm, smem);
         return sms * per_sm;
     });
     const size_t tiles = (n_rays + kM - 1) / kM;
     const int blocks = int(tiles < size_t(grid) ? tiles : size_t(grid));
-    shade_tc_kernel<<<blocks, kThreads, kSmemBytes, st>>>(
-        static_cast<const uint8_t*>(psi_tc), consts, acc, rgb, n_rays);
+    kernel<<<blocks, kThreads, smem, st>>>(static_cast<const uint8_t*>(psi_tc), consts, acc, rgb,
+                                           n_rays);
 }
 
 }  // namespace ngprt_dev
