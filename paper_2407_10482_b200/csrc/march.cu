@@ -853,6 +853,11 @@ __device__ __forceinline__ float& lane_row(float* scr, int base, int j) { return
 // (ngprt_render splits larger camera batches).
 constexpr uint32_t kIdxMask = NGPRT_EXIT_FLAG ? 0x7fffffffu : 0xffffffffu;
 // Per-lane ray state.
+// NGPRT_PROBE_REUSE: a lane keeps the last probe code and its level-1 voxel and
+// skips the load when the next marching point is in the same voxel (experiment).
+#ifndef NGPRT_PROBE_REUSE
+#define NGPRT_PROBE_REUSE 0
+#endif
 struct Lane {
     Ray ray;
     float t, t1;
@@ -860,6 +865,9 @@ struct Lane {
     float cd[3], fs[4], T;
     uint32_t n_march, n_occ, n_occ_acc, n_dist;
     uint32_t out_idx;
+#if NGPRT_PROBE_REUSE
+    uint32_t last_pidx, last_code;  // probe code of the last marching point's level-1 voxel
+#endif
     bool has_ray, pending;
 };
 
@@ -951,6 +959,9 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
     }
     s.T = 1.0f;
     s.n_march = s.n_occ = s.n_occ_acc = s.n_dist = 0;
+#if NGPRT_PROBE_REUSE
+    s.last_pidx = 0xffffffffu;
+#endif
     s.pending = false;
     s.has_ray = true;
 }
@@ -1045,7 +1056,19 @@ __device__ __forceinline__ bool march_point(const DevScene& sc, const MarchParam
     // level-k voxel = level-0 voxel >> k (exact: r_k = r0 / 2^k)
     const uint32_t pidx = probe_index(uint32_t(i0[0] >> 1), uint32_t(i0[1] >> 1), uint32_t(i0[2] >> 1), uint32_t(r1));
     NG_BOUNDS(pidx < uint32_t(r1) * uint32_t(r1) * uint32_t(r1));
+#if NGPRT_PROBE_REUSE
+    // consecutive marching points inside one level-1 voxel share its probe code
+    uint32_t code;
+    if (pidx == s.last_pidx) {
+        code = s.last_code;
+    } else {
+        code = ldg_probe(sc.probe + pidx);
+        s.last_pidx = pidx;
+        s.last_code = code;
+    }
+#else
     const uint32_t code = ldg_probe(sc.probe + pidx);
+#endif
     // occupancy_probe counters: e + 1 levels read (5 when level 0 decides).
     // Written branch-free so every empty point reaches next_step on one path.
     if constexpr (STATS) s.n_occ_acc += ((code >> 8) & 7u) + 1u;
@@ -1531,6 +1554,9 @@ __global__ void __launch_bounds__(kBlock) march_segments_kernel(
         s.out_idx |= ~kIdxMask;
 #endif
     s.n_march = s.n_occ = s.n_occ_acc = s.n_dist = 0;
+#if NGPRT_PROBE_REUSE
+    s.last_pidx = 0xffffffffu;
+#endif
     s.pending = false;
     int ns = 0, nt = 0;
     float t0, t1;
