@@ -434,3 +434,25 @@ def test_forced_fp16_storage_is_within_tolerance(ng, torch):
     got = rgb[0].cpu().numpy()
     assert np.abs(got - want_rgb).max() <= RGB_TOL
     assert psnr(got, want_rgb) >= PSNR_MIN
+
+
+@pytest.mark.parametrize("L", [2, 3, 4])
+@pytest.mark.parametrize("fusion", ["sum", "shared_att_inv", "separate_att_inv", "shared_att_v",
+                                    "separate_att_v"])
+@pytest.mark.parametrize("fp16_exact", [1, 0])
+def test_fusion_storage_matrix_matches_reference(ng, torch, L, fusion, fp16_exact):
+    """Every fusion mode x L = 2..4 x fp16 / f32 storage through the fast decode
+    (K1's fp16 and f32 variants): counters and exact-mode RGB bit-exact against
+    the compiled reference, tensor mode within the north_star tolerance."""
+    scene = ng.SynthScene(occupancy="toy", occ_base_res=64, L=L, L_C=48, fine_table_len=1 << 12,
+                          fusion_tag=fusion, fp16_exact=fp16_exact, psi_bias_scale=0.1)
+    dev = ng.Scene(scene)
+    assert dev.info().storage == (2 if fp16_exact else 1)
+    cam = ng.cameras(5, 40, 32)[L]
+    rgb, st = gpu_render(ng, torch, dev, cam, ng.Opts(mlp="exact"))
+    want_rgb, want_st = ref_scene(scene.desc_ptr).render(cam, ng.Opts(mlp="exact").to_c())
+    assert np.array_equal(st, want_st)
+    assert np.array_equal(rgb.view(np.uint32), want_rgb.view(np.uint32))
+    t_rgb, t_st = gpu_render(ng, torch, dev, cam, ng.Opts(mlp="tensor"))
+    assert np.array_equal(t_st, want_st)
+    assert np.abs(t_rgb - want_rgb).max() <= RGB_TOL
