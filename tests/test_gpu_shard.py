@@ -210,3 +210,19 @@ def test_duplicate_coarse_keys_keep_the_first_row(ng, torch):
     assert np.array_equal(bits(rgb[0]), want_rgb.view(np.uint32))
     assert np.array_equal(st[0].cpu().numpy().view(np.uint32), want_st)
     assert np.array_equal(bits(rgb), bits(base))
+
+
+def test_sharded_host_buffer_calls_match_device_calls(ng, torch, small):
+    """ngprt_render_host and ngprt_render_host_async accept sharded options and
+    return the same compact buffer as the device-buffer call."""
+    _, dev = small
+    cams = ng.cameras(3, 72, 40)
+    o = ng.Opts(mlp="exact", shard_world=3, shard_rank=1, shard_tile=16)
+    want = ng.render(dev, cams, o).cpu().numpy()
+    got = ng.render_host(dev, cams, o)
+    assert got.shape == want.shape
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    out = np.zeros_like(want)
+    ng.render_host_async(dev, cams, out, o)
+    ng.render_host_wait(dev)
+    assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
