@@ -499,6 +499,17 @@ namespace {
 // access-policy window").
 void set_l2_window(const ngprt_scene* s, cudaStream_t st, cudaStreamAttrValue* saved) {
     cudaStreamGetAttribute(st, cudaStreamAttributeAccessPolicyWindow, saved);
+    // tuning hooks: NGPRT_L2_WINDOW=0 renders without the window, NGPRT_L2_HIT_RATIO
+    // scales the persisting fraction of it
+    static const int window_on = [] {
+        const char* e = std::getenv("NGPRT_L2_WINDOW");
+        return e ? std::atoi(e) : 1;
+    }();
+    static const float ratio_scale = [] {
+        const char* e = std::getenv("NGPRT_L2_HIT_RATIO");
+        return e ? float(std::atof(e)) : 1.0f;
+    }();
+    if (!window_on) return;
     int max_win = 0, max_persist = 0;
     cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
@@ -512,7 +523,7 @@ void set_l2_window(const ngprt_scene* s, cudaStream_t st, cudaStreamAttrValue* s
     cudaStreamAttrValue v{};
     v.accessPolicyWindow.base_ptr = s->fine_block;
     v.accessPolicyWindow.num_bytes = win;
-    v.accessPolicyWindow.hitRatio = std::min(1.0f, float(double(cur) / double(win)));
+    v.accessPolicyWindow.hitRatio = std::min(1.0f, ratio_scale * float(double(cur) / double(win)));
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
