@@ -511,17 +511,16 @@ void set_l2_window(const ngprt_scene* s, cudaStream_t st, cudaStreamAttrValue* s
         return e ? float(std::atof(e)) : 1.0f;
     }();
     if (!window_on) return;
-    int max_win = 0, max_persist = 0, l2 = 0;
+    int max_win = 0, max_persist = 0;
     cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s->device);
     if (max_win <= 0 || max_persist <= 0 || !s->fine_block) return;
-    // Persist the fine tables only while they take at most a third of L2: above
-    // that the persisting lines cost the coarse rows more hits than they save
-    // (measured: c1's 32 MB block 0.233 -> 0.229 ms with the window;
-    // c3's 64 MB 3.36 -> 3.41 ms, c2's 128 MB 0.238 -> 0.247 ms), and LRU keeps the
-    // hot fine rows resident by itself.
-    if (window_on == 1 && l2 > 0 && s->fine_block_bytes > size_t(l2) / 3) return;
+    // Persist the fine tables only while they fit in half of the persisting
+    // set-aside (41 MB on B200): above that the persisting lines cost the coarse
+    // rows more hits than they save (measured: c1's 32 MB block
+    // 0.233 -> 0.229 ms with the window; c3's 64 MB 3.36 -> 3.41 ms, c2's 128 MB
+    // 0.238 -> 0.247 ms), and LRU keeps the hot fine rows resident by itself.
+    if (window_on == 1 && s->fine_block_bytes > size_t(max_persist) / 2) return;
     const size_t win = std::min<size_t>(s->fine_block_bytes, size_t(max_win));
     size_t cur = 0;
     cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
