@@ -852,6 +852,11 @@ __device__ __forceinline__ float& lane_row(float* scr, int base, int j) { return
 // Lane::out_idx bit 31 is that flag; pixel indices of one launch stay below 2^31
 // (ngprt_render splits larger camera batches).
 constexpr uint32_t kIdxMask = NGPRT_EXIT_FLAG ? 0x7fffffffu : 0xffffffffu;
+// NGPRT_STREAM_HINTS (experiment): 1 = evict-first stores of the per-ray
+// accumulators, 2 = evict-first loads of the K0 ray records.
+#ifndef NGPRT_STREAM_HINTS
+#define NGPRT_STREAM_HINTS 0
+#endif
 // Per-lane ray state.
 // NGPRT_PROBE_REUSE: a lane keeps the last probe code and its level-1 voxel and
 // skips the load when the next marching point is in the same voxel (experiment).
@@ -900,7 +905,15 @@ __device__ __forceinline__ void write_result(const MarchParams& p, const Lane& s
                       valid ? s.ray.d[2] : 0.f, valid ? 1.f : 0.f);
     const uint32_t idx = s.out_idx & kIdxMask;
     NG_BOUNDS(idx < p.n_slots);
+#if NGPRT_STREAM_HINTS & 1
+    // the 48 B per-ray accumulator is read once, by K2: evict-first in L2 so it
+    // does not push the gathered rows out
+    __stcs(&p.acc[idx].a, r.a);
+    __stcs(&p.acc[idx].b, r.b);
+    __stcs(&p.acc[idx].c, r.c);
+#else
     p.acc[idx] = r;
+#endif
     if (p.stats) {
         ngprt_ray_stats st;
         st.marching = s.n_march;
@@ -936,8 +949,13 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
         s.out_idx = (cam * p.h + py) * p.w + px;
     }
     NG_BOUNDS(s.out_idx < p.n_slots);
+#if NGPRT_STREAM_HINTS & 2
+    const float4 a = __ldcs(p.rays + 2 * size_t(s.out_idx));  // read once: evict-first
+    const float4 b = __ldcs(p.rays + 2 * size_t(s.out_idx) + 1);
+#else
     const float4 a = __ldg(p.rays + 2 * size_t(s.out_idx));
     const float4 b = __ldg(p.rays + 2 * size_t(s.out_idx) + 1);
+#endif
     if (!(b.w >= 0.0f)) return;  // K0 wrote the result (generate_rays/clip_to_roi miss)
     s.ray.o[0] = a.x; s.ray.o[1] = a.y; s.ray.o[2] = a.z;
     s.ray.d[0] = b.x; s.ray.d[1] = b.y; s.ray.d[2] = b.z;
