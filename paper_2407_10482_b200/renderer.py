@@ -424,6 +424,8 @@ def render_host(scene: Scene, cams, opts: Opts | None = None, out=None, stats=No
     elif out.dtype != np.float32 or not out.flags.c_contiguous or out.size < n * 3 * int(np.prod(shp)):
         raise ValueError("out must be a C-contiguous float32 array of at least "
                          f"{(n, *shp, 3)} elements")
+    if stats is not None and (not stats.flags.c_contiguous or stats.nbytes < 16 * n * int(np.prod(shp))):
+        raise ValueError(f"stats must be a C-contiguous array of at least {(n, *shp, 4)} u32")
     o = opts.to_c()
     check(lib().ngprt_render_host(scene.handle, cams, n, C.byref(o), out.ctypes.data,
                                   stats.ctypes.data if stats is not None else None),
@@ -436,6 +438,11 @@ def render_host_async(scene: Scene, cams, out, opts: Opts | None = None, stats=N
     `out` (and `stats`) must stay alive, ideally pinned, until render_host_wait."""
     opts = opts or Opts()
     cams = camera_array(cams)
+    need = len(cams) * int(np.prod(_out_shape(cams, opts)))
+    if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < 3 * need:
+        raise ValueError(f"out must be a C-contiguous float32 array of at least {3 * need} elements")
+    if stats is not None and (not stats.flags.c_contiguous or stats.nbytes < 16 * need):
+        raise ValueError(f"stats must be a C-contiguous array of at least {16 * need} bytes")
     o = opts.to_c()
     check(lib().ngprt_render_host_async(scene.handle, cams, len(cams), C.byref(o), out.ctypes.data,
                                         stats.ctypes.data if stats is not None else None),
