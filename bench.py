@@ -627,7 +627,7 @@ def run_ours(args):
                          "l2_gbs": (l2_traffic / (k1_avg / 1e3) / 1e9) if l2_traffic else None,
                          "dram_gbs": (traffic / (k1_avg / 1e3) / 1e9) if traffic else None,
                          "binding_ceiling": binding_ceiling(tj, k1_avg, ceilings)},
-            "k2_tensor": {"kernel": "shade_tc_kernel (K2)" if args.mlp == "tensor" else "shade_exact_kernel",
+            "k2_tensor": {"kernel": "shade_tc_pipe_kernel (K2)" if args.mlp == "tensor" else "shade_exact_kernel",
                           "shaded_rays": int(shaded), "flop_per_launch": k2_flop,
                           "achieved_tflops": k2_flop / (k2_avg * 1e-3) / 1e12,
                           "peak_tflops": load_tensor_peak(),
