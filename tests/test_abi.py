@@ -92,3 +92,24 @@ def test_expf_port_table_matches_host_libm():
     assert after[6:9] == (float.fromhex("0x1.c6af84b912394p-20"),
                           float.fromhex("0x1.ebfce50fac4f3p-13"),
                           float.fromhex("0x1.62e42ff0c52d6p-6"))
+
+
+def test_multi_and_shard_entry_points_validate_on_cpu(ng):
+    """The multi-device and sharding entry points validate their arguments and fail
+    loudly (no device here) instead of crashing; ngprt_shard_pixels is pure host
+    arithmetic."""
+    import ctypes as C
+    L = ng.lib()
+    h = C.c_void_p()
+    assert L.ngprt_multi_create(None, None, 0, C.byref(h)) == ng._abi.EINVAL
+    d = ng._abi.SceneDesc()
+    d.L = 7
+    devs = (C.c_int * 1)(0)
+    assert L.ngprt_multi_create(C.byref(d), devs, 1, C.byref(h)) == ng._abi.EINVAL
+    assert b"L out of range" in L.ngprt_last_error()
+    assert L.ngprt_multi_uses_nccl(None) == 0
+    assert L.ngprt_multi_scene(None, 0) is None
+    # ceil(60 tiles / 7) = 9 tiles of 32 x 32 per rank for a 300 x 190 window
+    assert L.ngprt_shard_pixels(300, 190, 7, 32) == 9 * 32 * 32
+    assert L.ngprt_shard_pixels(300, 190, 0, 0) == 60 * 32 * 32  # world 0 => 1, tile 0 => 32
+    assert L.ngprt_shard_assemble(None, 1, 1, 8, 8, 8, 3, None, None) == ng._abi.EINVAL
