@@ -21,6 +21,12 @@ namespace {
 
 constexpr uint16_t kInf = 0xFFFF;
 
+// NGPRT_DT_UNSTAGED (experiment): the envelope sweep reads its column through L1
+// instead of staging it in shared memory (half the shared memory per column).
+#ifndef NGPRT_DT_UNSTAGED
+#define NGPRT_DT_UNSTAGED 0
+#endif
+
 __device__ __forceinline__ bool get_bit(const uint32_t* g, int res, int x, int y, int z) {
     const size_t i = size_t(x) + size_t(res) * (size_t(y) + size_t(res) * size_t(z));
     return (g[i >> 5] >> (i & 31)) & 1u;
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
                                                          uint8_t* __restrict__ out8) {
     extern __shared__ __align__(16) uint16_t colbuf[];  // [r][C] column, then s [r][C], t [r][C]
     const int C = blockDim.x, tid = threadIdx.x;
-    IT* s = reinterpret_cast<IT*>(colbuf + size_t(r) * C) + tid;
+    IT* s = reinterpret_cast<IT*>(colbuf + (NGPRT_DT_UNSTAGED ? 0 : size_t(r) * C)) + tid;
     IT* t = s + size_t(r) * C;
     const size_t col = blockIdx.x * size_t(C) + tid;
     const bool live = col < size_t(r) * r;
@@ -196,6 +202,65 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
     const size_t x = col % size_t(r), o = col / size_t(r);
     const size_t base = AXIS == 1 ? o * size_t(r) * r + x : o * size_t(r) + x;
     const size_t stride = AXIS == 1 ? size_t(r) : size_t(r) * r;
+#if NGPRT_DT_UNSTAGED
+    // variant: no column staging; the sweep reads the column through L1 (the next
+    // element prefetched one step ahead), the stacks alone take shared memory
+    if (!live) return;
+    const uint16_t* gcol = in + base;
+    auto G = [&](int u) -> int { return __ldg(gcol + size_t(u) * stride); };
+    int q = 0, sq = 0, tq = 0;
+    s[0] = 0;
+    t[0] = 0;
+    int gs = G(0);
+    int gnext = r > 1 ? G(1) : 0;
+    for (int u = 1; u < r; ++u) {
+        const int gu = gnext;
+        if (u + 1 < r) gnext = G(u + 1);
+        while (q >= 0 && cheb_f(tq, sq, gs) > cheb_f(tq, u, gu)) {
+            --q;
+            if (q >= 0) {
+                sq = s[q * C];
+                tq = t[q * C];
+                gs = G(sq);
+            }
+        }
+        if (q < 0) {
+            q = 0;
+            sq = u;
+            tq = 0;
+            s[0] = IT(u);
+            t[0] = 0;
+            gs = gu;
+        } else {
+            const int w = 1 + cheb_sep(sq, u, gs, gu);
+            if (w < r) {
+                ++q;
+                sq = u;
+                tq = w;
+                s[q * C] = IT(u);
+                t[q * C] = IT(w);
+                gs = gu;
+            }
+        }
+    }
+    for (int u = r - 1; u >= 0; --u) {
+        const int h = cheb_f(u, sq, gs);
+        const size_t i = base + size_t(u) * stride;
+        if (FINAL) {
+            const int gg = h == 0 ? 0 : h - 1;  // occupancy.hpp:188-192
+            out8[i] = uint8_t(gg < 255 ? gg : 255);
+        } else {
+            out[i] = uint16_t(h < int(kInf) ? h : int(kInf));
+        }
+        if (u == tq && q > 0) {
+            --q;
+            sq = s[q * C];
+            tq = t[q * C];
+            gs = G(sq);
+        }
+    }
+    return;
+#endif
     uint16_t* g = colbuf + tid;
     if (r % C == 0 && C % 8 == 0) {
         // the CTA's C columns are C consecutive x of one row: stage the r segments of
@@ -328,11 +393,11 @@ void launch_distance_grid(const uint32_t* occ, int r, uint16_t* a, uint16_t* b, 
         return 1;
     });
     if (r <= 256) {  // 64 columns per CTA, u8 stack indices: r x 64 x 4 B (<= 64 KB)
-        const size_t sm = size_t(r) * 64 * 4;
+        const size_t sm = size_t(r) * 64 * (NGPRT_DT_UNSTAGED ? 2 : 4);
         dt_envelope_kernel<1, false, uint8_t><<<blocks_for(rows, 64), 64, sm, st>>>(a, r, b, nullptr);
         dt_envelope_kernel<2, true, uint8_t><<<blocks_for(rows, 64), 64, sm, st>>>(b, r, nullptr, out);
     } else if (r <= 1024) {  // 16 columns per CTA, u16 stack indices: r x 16 x 6 B (<= 96 KB)
-        const size_t sm = size_t(r) * 16 * 6;
+        const size_t sm = size_t(r) * 16 * (NGPRT_DT_UNSTAGED ? 4 : 6);
         dt_envelope_kernel<1, false, uint16_t><<<blocks_for(rows, 16), 16, sm, st>>>(a, r, b, nullptr);
         dt_envelope_kernel<2, true, uint16_t><<<blocks_for(rows, 16), 16, sm, st>>>(b, r, nullptr, out);
     } else {  // beyond the envelope stacks' size: the outward search
