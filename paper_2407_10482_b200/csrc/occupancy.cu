@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
     // variant: no column staging; the sweep reads the column through L1 (the next
     // element prefetched one step ahead), the stacks alone take shared memory
     if (!live) return;
+    {
     const uint16_t* gcol = in + base;
     auto G = [&](int u) -> int { return __ldg(gcol + size_t(u) * stride); };
     int q = 0, sq = 0, tq = 0;
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(64) dt_envelope_kernel(const uint16_t* __restr
         }
     }
     return;
+    }
 #endif
     uint16_t* g = colbuf + tid;
     if (r % C == 0 && C % 8 == 0) {
