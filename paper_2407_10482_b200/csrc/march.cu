@@ -1345,12 +1345,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks<L, F16>) march_kernel(const
                     break;
                 }
                 if (s.pending) break;
-                // experiment (MarchParams::burst_stop): end the burst for the whole
-                // warp once enough lanes are parked (lanes that left the loop are
-                // counted as parked: an approximation, only the schedule changes)
-                if (p.burst_stop &&
-                    __popc(parked) + __popc(stepping & ~__activemask()) >= p.burst_stop)
-                    break;
             }
         }
     }

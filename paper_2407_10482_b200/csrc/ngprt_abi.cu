@@ -633,11 +633,6 @@ ngprt_status render_impl(const ngprt_scene* s, const ngprt_camera* cams, int n_c
         }();
         p.decode_min = dmin;
         p.step_burst = burst;
-        static const int burst_stop = [] {  // experiment hook, off by default
-            const char* e = std::getenv("NGPRT_BURST_STOP");
-            return e ? std::max(0, std::min(32, std::atoi(e))) : 0;
-        }();
-        p.burst_stop = burst_stop;
         // Tensor-MLP mode tolerates 1e-3 on RGB: K1 then accumulates the colour
         // channels with FMA (density / attention / transmittance stay exact, so
         // the per-ray counters do too). NGPRT_FAST_COLOR=0 keeps them exact.

@@ -83,7 +83,6 @@ struct MarchParams {
     float step;
     int use_grid, max_step_rule, early_stop, keep_level;
     int decode_min, step_burst;  // K1 warp scheduling policy (tunable, see march.cu)
-    int burst_stop;              // experiment: end a step burst at this many parked lanes (0 = off)
     int fast_color;              // tensor-MLP mode: colour channels with FMA (see march.cu)
     RayAcc* acc;              // n_cams x h x w
     ngprt_ray_stats* stats;   // nullable, n_cams x h x w
