@@ -125,3 +125,27 @@ def test_loaded_file_renders_like_the_reference(ng, saved):
     want_rgb, want_st = rs.render(cam, opts.to_c(), nthreads=8)
     assert np.array_equal(st[0].cpu().numpy().view(np.uint32), want_st)
     assert np.array_equal(rgb[0].cpu().numpy().view(np.uint32), want_rgb.view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_full_scale_bench_scene_through_the_reference_file(ng, tmp_path):
+    """The bench scene itself (config 3: 512^3 pyramid, 256^3 distance grid, L_C =
+    512, 2^21-row tables, ~19 M coarse rows) written by the reference's save_baked,
+    loaded by ngprt_scene_load and rendered at 1080p: counters and exact-mode RGB
+    bit-exact against the reference rendering the same BakedScene."""
+    import torch
+    R = ref()
+    assert R is not None, "compiled reference (oracle/_ref) required"
+    synth = ng.SynthScene(**dict(ng.CONFIGS["c3_1080p"]))
+    rs = CpuScene(synth.desc_ptr, "ref")
+    path = tmp_path / "c3.ngrt"
+    assert R.ref_save_baked(rs.h, str(path).encode()) == 0
+    dev = ng.Scene(ng.BakedFile(path))
+    assert dev.info().storage == 2  # the file's f32 values are fp16-exact: lossless fp16 rows
+    cam = ng.cameras(64, 1920, 1080)[13]
+    rgb, st = ng.render(dev, [cam], ng.Opts(mlp="exact"), stats=True)
+    torch.cuda.synchronize()
+    want_rgb, want_st = rs.render(cam, ng.Opts(mlp="exact").to_c())
+    assert np.array_equal(st[0].cpu().numpy().view(np.uint32), want_st)
+    assert np.array_equal(rgb[0].cpu().numpy().view(np.uint32), want_rgb.view(np.uint32))
+    assert (want_st[..., 1] > 0).mean() > 0.5  # most rays reach occupied points
