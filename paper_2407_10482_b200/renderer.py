@@ -496,6 +496,8 @@ def shard_assemble(shards, world: int, n_cams: int, width: int, height: int, til
     if shards.element_size() != 4:
         raise ValueError("shards must have 4-byte elements (f32 RGB or u32 counters)")
     s = stream if stream is not None else torch.cuda.current_stream(shards.device)
-    check(lib().ngprt_shard_assemble(shards.data_ptr(), world, n_cams, width, height, tile, channels,
-                                     out.data_ptr(), s.cuda_stream), "ngprt_shard_assemble")
+    with torch.cuda.device(shards.device):  # the kernel launches on the current device
+        check(lib().ngprt_shard_assemble(shards.data_ptr(), world, n_cams, width, height, tile,
+                                         channels, out.data_ptr(), s.cuda_stream),
+              "ngprt_shard_assemble")
     return out
