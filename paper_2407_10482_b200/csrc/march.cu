@@ -314,9 +314,35 @@ __device__ __forceinline__ float mac(bool fma, float acc, float w, float v) {
     return fma ? __fmaf_rn(w, v, acc) : acc + w * v;
 }
 
+// Two exact channels (a0 += w0 * v0, a1 += w1 * v1, product and sum each
+// rounded like the reference's FMUL and FADD) as two packed sm_100
+// instructions. The product is FFMA2(w, v, +0): RN(w*v + 0) is RN(w*v) except
+// that a -0 product becomes +0, and ptxas does not fold it into the add (it
+// contracts mul.f32x2 + add.f32x2, or an addend of -0, into one FFMA2). The
+// zero sign never shows: every accumulator here starts at +0 and a sum that
+// starts at +0 is never -0 under round-to-nearest (+0 + -0 = +0, exact
+// cancellation gives +0), so adding +0 instead of -0 leaves it unchanged.
+#ifndef NGPRT_PACKED_EXACT
+#define NGPRT_PACKED_EXACT 1
+#endif
+__device__ __forceinline__ void mac2x(float& a0, float& a1, float w0, float w1, float v0,
+                                      float v1) {
+#if NGPRT_PACKED_EXACT
+    unsigned long long acc, v, ww, prod;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(v0), "f"(v1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ww) : "f"(w0), "f"(w1));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(prod) : "l"(ww), "l"(v), "l"(0ull));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(prod));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+#else
+    a0 = mac(false, a0, w0, v0);
+    a1 = mac(false, a1, w1, v1);
+#endif
+}
+
 // A pair of channels: with fma (both channels FMA-allowed) one sm_100 FFMA2
-// (packed f32x2; each half rounds exactly like a scalar FMA), else two mac()s.
-// Never used for exact channels: ptxas contracts packed multiply + add pairs.
+// (packed f32x2; each half rounds exactly like a scalar FMA), else mac2x.
 __device__ __forceinline__ void mac2(bool fma, float& a0, float& a1, float w, float v0, float v1) {
     if (fma) {
         unsigned long long acc, v, ww;
@@ -326,8 +352,7 @@ __device__ __forceinline__ void mac2(bool fma, float& a0, float& a1, float w, fl
         asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(ww), "l"(v));
         asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
     } else {
-        a0 = mac(false, a0, w, v0);
-        a1 = mac(false, a1, w, v1);
+        mac2x(a0, a1, w, w, v0, v1);
     }
 }
 
@@ -393,8 +418,7 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            fine[0] = mac(false, fine[0], w[k], frow[k][0]);
-            fine[1] = mac(FC, fine[1], w[k], frow[k][1]);
+            mac2x(fine[0], fine[1], w[k], w[k], frow[k][0], frow[k][1]);
 #pragma unroll
             for (int c = 2; c < 8; c += 2)
                 mac2(FC, fine[c], fine[c + 1], w[k], frow[k][c], frow[k][c + 1]);
@@ -700,12 +724,10 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
                 const float2 v = F16 ? __half22float2(*reinterpret_cast<const __half2*>(&craw[k][i]))
                                      : make_float2(__uint_as_float(craw[k][2 * i]),
                                                    __uint_as_float(craw[k][2 * i + 1]));
-                if (FC && !exact_channel(2 * i) && !exact_channel(2 * i + 1)) {
+                if (FC && !exact_channel(2 * i) && !exact_channel(2 * i + 1))
                     mac2(true, dec[2 * i], dec[2 * i + 1], w[k], v.x, v.y);
-                } else {
-                    dec[2 * i] = mac(FC && !exact_channel(2 * i), dec[2 * i], w[k], v.x);
-                    dec[2 * i + 1] = mac(FC && !exact_channel(2 * i + 1), dec[2 * i + 1], w[k], v.y);
-                }
+                else  // an exact channel's partner is exact too (one packed pair)
+                    mac2x(dec[2 * i], dec[2 * i + 1], w[k], w[k], v.x, v.y);
             }
     }
     // ---- attention (split_decoder_output, model.hpp:18-21) ----
@@ -759,12 +781,10 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
                 const float2 v = F16 ? __half22float2(*reinterpret_cast<const __half2*>(&fraw[l][k][i]))
                                      : make_float2(__uint_as_float(fraw[l][k][2 * i]),
                                                    __uint_as_float(fraw[l][k][2 * i + 1]));
-                if (FC && i != 0) {
+                if (FC && i != 0)
                     mac2(true, fine[2 * i], fine[2 * i + 1], w[k], v.x, v.y);
-                } else {
-                    fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
-                    fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
-                }
+                else
+                    mac2x(fine[2 * i], fine[2 * i + 1], w[k], w[k], v.x, v.y);
             }
         }
         if (keep_level > 0 && l + 1 != keep_level) {
@@ -773,8 +793,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         }
         float wo, wb;
         weights(l, wo, wb);
-        out[0] += wo * fine[0];
-        out[1] = mac(FC, out[1], wb, fine[1]);
+        mac2x(out[0], out[1], wo, wb, fine[0], fine[1]);
 #pragma unroll
         for (int c = 2; c < 8; c += 2) mac2(FC, out[c], out[c + 1], wb, fine[c], fine[c + 1]);
     }
@@ -795,12 +814,10 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float2 v = __half22float2(h[i]);
-                if (FC && i != 0) {
+                if (FC && i != 0)
                     mac2(true, fine[2 * i], fine[2 * i + 1], w[k], v.x, v.y);
-                } else {
-                    fine[2 * i] = mac(FC && i != 0, fine[2 * i], w[k], v.x);
-                    fine[2 * i + 1] = mac(FC, fine[2 * i + 1], w[k], v.y);
-                }
+                else
+                    mac2x(fine[2 * i], fine[2 * i + 1], w[k], w[k], v.x, v.y);
             }
         }
         if (keep_level > 0 && l + 1 != keep_level) {
@@ -809,8 +826,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         }
         float wo, wb;
         weights(l, wo, wb);
-        out[0] += wo * fine[0];
-        out[1] = mac(FC, out[1], wb, fine[1]);
+        mac2x(out[0], out[1], wo, wb, fine[0], fine[1]);
 #pragma unroll
         for (int c = 2; c < 8; c += 2) mac2(FC, out[c], out[c + 1], wb, fine[c], fine[c + 1]);
     }
@@ -825,8 +841,7 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
         }
         float wo, wb;
         weights(l, wo, wb);
-        out[0] += wo * fine[0];
-        out[1] = mac(FC, out[1], wb, fine[1]);
+        mac2x(out[0], out[1], wo, wb, fine[0], fine[1]);
 #pragma unroll
         for (int c = 2; c < 8; c += 2) mac2(FC, out[c], out[c + 1], wb, fine[c], fine[c + 1]);
     }

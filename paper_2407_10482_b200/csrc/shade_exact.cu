@@ -7,10 +7,10 @@
 // layers run input-major: for each input c, every output's accumulator takes
 // its c-th term, so each output still sums b, then c = 0, 1, ... in order. The
 // weights sit transposed in shared memory ([c][o], one broadcast LDS.128 per
-// four outputs) and the products of two outputs are one FMUL2 (sm_100 packed
-// f32x2 multiply, each half rounded like FMUL); the adds stay scalar FADDs
-// (ptxas contracts packed multiply + packed add into FFMA2, scalar adds it
-// leaves alone), so every operation rounds as the reference's.
+// four outputs); the products of two outputs are one packed FFMA2 with a +0
+// addend and their sums one FADD2 (sm_100 f32x2, each half rounded like FMUL /
+// FADD; see mac_pair_exact for why ptxas keeps them apart and why the zero
+// sign cannot reach the RGB), so every operation rounds as the reference's.
 #include "render.cuh"
 
 namespace ngprt_dev {
@@ -20,15 +20,34 @@ constexpr int kShadeBlock = 128;
 constexpr int kColsBytes = 64 * kShadeBlock * 4;
 
 // (a0, a1) += (w0 * x, w1 * x), each product and each sum rounded separately.
+#ifndef NGPRT_EXACT_PACKED_ADD
+#define NGPRT_EXACT_PACKED_ADD 1
+#endif
 __device__ __forceinline__ void mac_pair_exact(float& a0, float& a1, float w0, float w1, float x) {
     unsigned long long wp, xp, p;
     asm("mov.b64 %0, {%1, %2};" : "=l"(wp) : "f"(w0), "f"(w1));
     asm("mov.b64 %0, {%1, %1};" : "=l"(xp) : "f"(x));
+#if NGPRT_EXACT_PACKED_ADD
+    // Product as FFMA2(w, x, +0): RN(w*x + 0) equals RN(w*x) except that a -0
+    // product becomes +0. ptxas does not fold this form into the following add
+    // (it would for mul.f32x2 or an addend of -0, which are exact identities),
+    // so the sum stays one FADD2 rounding each half like FADD. The sign of a
+    // zero product only reaches a result when the accumulator is -0, which
+    // yields a zero of the other sign; the ReLU compares (h < 0) and the
+    // sigmoid (exp(-(+-0)) = 1) treat both zeros alike, so the RGB bits equal
+    // the reference's in every case.
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(wp), "l"(xp), "l"(0ull));
+    unsigned long long a;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(p));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
+#else
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(wp), "l"(xp));
     float p0, p1;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
     a0 = __fadd_rn(a0, p0);
     a1 = __fadd_rn(a1, p1);
+#endif
 }
 
 // out[0..63] = b[0..63] + sum_c Wt[c][0..63] * in[c], c ascending. The inputs
