@@ -734,7 +734,7 @@ extern "C" ngprt_status ngprt_bake(const ngprt_model_desc* md, const uint64_t* t
             launch_pyramid_level(levels[k - 1], render_res >> (k - 1), levels[k], nullptr);
         }
         uint8_t* dist = db.alloc<uint8_t>(size_t(256) * 256 * 256);
-        uint16_t* ta = db.alloc<uint16_t>(size_t(256) * 256 * 256);
+        uint16_t* ta = db.alloc<uint16_t>(size_t(256) * 256 * 256 + kDistScratchPad / 2);
         uint16_t* tb = db.alloc<uint16_t>(size_t(256) * 256 * 256);
         launch_distance_grid(levels[1], 256, ta, tb, dist, nullptr);
         check_cuda("bake: pyramid / distance grid");

@@ -394,7 +394,7 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
             int k = 0;
             while (ds.occ_res[k] != int(r)) ++k;
             uint16_t *a, *b;
-            NG_TRY(cudaMallocAsync(&a, n * 2, st));
+            NG_TRY(cudaMallocAsync(&a, n * 2 + kDistScratchPad, st));
             NG_TRY(cudaMallocAsync(&b, n * 2, st));
             launch_distance_grid(ds.occ[k], int(r), a, b, g, st);
             NG_TRY(cudaGetLastError());
@@ -933,7 +933,7 @@ ngprt_status ngprt_build_distance_grid(const uint64_t* occ, uint32_t res, uint8_
     const size_t n = size_t(res) * res * res;
     keep_pool_mapped();
     uint16_t *a, *b;
-    NG_CUDA(cudaMallocAsync(&a, n * 2, st));
+    NG_CUDA(cudaMallocAsync(&a, n * 2 + kDistScratchPad, st));
     NG_CUDA(cudaMallocAsync(&b, n * 2, st));
     launch_distance_grid(reinterpret_cast<const uint32_t*>(occ), int(res), a, b, out, st);
     NG_CUDA(cudaGetLastError());

@@ -118,6 +118,8 @@ void pack_psi_tc(const float* psi_host_packed, void* psi_tc_host);
 
 // K3/K4: occupancy structures.
 void launch_pyramid_level(const uint32_t* src, int src_res, uint32_t* dst, cudaStream_t st);
+// tmp_a: res^3 x 2 + kDistScratchPad bytes, tmp_b: res^3 x 2 bytes.
+constexpr size_t kDistScratchPad = 64;
 void launch_distance_grid(const uint32_t* occ, int res, uint16_t* tmp_a, uint16_t* tmp_b,
                           uint8_t* out, cudaStream_t st);
 void launch_scatter_coarse(const unsigned long long* keys, const float* rows, size_t n, int w,

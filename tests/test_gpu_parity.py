@@ -141,6 +141,57 @@ def test_distance_grid_single_voxel(ng, torch):
     assert crc(ng, out) == G["dt_single_voxel"]["crc"]
 
 
+DT_U8_GRIDS = [(256, 0.0, 21), (256, 2e-7, 22), (256, 1e-4, 23), (256, 0.3, 24),
+               (200, 1e-6, 25), (96, 0.002, 26), (33, 0.05, 27), (4, 0.3, 28), ("corner", 0, 0),
+               ("diagonal", 0, 0)]
+_DT_WANT = {}
+
+
+def _dt_case(ng, R, res, dens, seed):
+    key = (res, dens, seed)
+    if res == "corner":  # one voxel at (0,0,0): D = 255 at the far corner (G = 254)
+        words = np.zeros(256 ** 3 // 64, np.uint64)
+        words[0] = np.uint64(1)
+        res = 256
+    elif res == "diagonal":  # the plane x = 2y at z < 128: slope-2 ramps, long deques
+        bits = np.zeros((256, 256, 256), np.uint8)  # z, y, x
+        y = np.arange(128)
+        bits[:128, y, 2 * y] = 1
+        words = np.zeros(256 ** 3 // 64, np.uint64)
+        words.view(np.uint8)[:] = np.packbits(bits.ravel(), bitorder="little")
+        res = 256
+    else:
+        words = random_grid_words(ng, res, dens, seed)
+    if key not in _DT_WANT:
+        want = np.zeros(res ** 3, np.uint8)
+        R.ref_build_distance_grid(words.ctypes.data, res, want.ctypes.data)
+        _DT_WANT[key] = want
+    return words, res, _DT_WANT[key]
+
+
+@pytest.mark.parametrize("depth", [None, "16", "1", "2"])
+def test_distance_grid_u8_passes_match_reference(ng, torch, monkeypatch, depth):
+    """K4's u8 passes (r <= 256: distances saturated at 255, the all-empty grid
+    flagged by pass X) equal the compiled reference's build_distance_grid
+    (occupancy.hpp:136-194) byte for byte on empty, near-empty (distances up to
+    255), dense, diagonal-plane, non-multiple-of-32 and tiny grids. Default: the
+    range-minimum kernel where r is a multiple of 32, the deque kernel
+    elsewhere. NGPRT_DT_RING forces the deque kernel everywhere, with the
+    default ring (16 entries; the diagonal plane overflows it) and with rings
+    of 1 and 2 entries (every or most columns redone with the global deque)."""
+    from checkers import ref
+    R = ref()
+    assert R is not None, "compiled reference (oracle/_ref) required"
+    if depth:
+        monkeypatch.setenv("NGPRT_DT_RING", depth)
+    for res, dens, seed in DT_U8_GRIDS:
+        words, r, want = _dt_case(ng, R, res, dens, seed)
+        got = ng.build_distance_grid(torch.from_numpy(words.view(np.int64)).cuda(), r).cpu().numpy()
+        assert np.array_equal(got, want), (res, dens, depth, int((got != want).sum()))
+        if res == "corner":
+            assert want[-1] == 254
+
+
 def test_pyramid_matches_oracle_on_random_grids(ng, torch):
     from checkers import oracle
     O = oracle()

@@ -3,13 +3,17 @@ line info, aggregating warp instructions / thread instructions / stall samples
 per source line of one kernel.
 
   python tools/ncu_source_lines.py <lib.so> <report.ncu-rep> <mangled-name-fragment> <out.tsv>
+
+NCU_CUBIN selects the cubin (default "march"), NCU_KERNEL the report's kernel
+block by a substring of its demangled name (default: the mangled fragment's
+base name; set it when several instantiations were captured).
 """
 import csv, re, sys, collections, subprocess, os, glob
 lib, rep, fn = sys.argv[1], sys.argv[2], sys.argv[3]
 d = f"/tmp/cmp/{os.path.basename(lib)}"
 os.makedirs(d, exist_ok=True)
 subprocess.run(f"cd {d} && cuobjdump -xelf all {lib} >/dev/null 2>&1", shell=True)
-cub = [c for c in glob.glob(d+"/*.cubin") if "march" in c][0]
+cub = [c for c in glob.glob(d+"/*.cubin") if os.environ.get("NCU_CUBIN", "march") in c][0]
 txt = subprocess.run(["nvdisasm","-gi",cub],capture_output=True,text=True).stdout.split("\n")
 start=None
 for i,l in enumerate(txt):
@@ -35,7 +39,7 @@ blocks.append(len(rows))
 sel=None
 for bi in range(len(blocks)-1):
     name=rows[blocks[bi]][1] if len(rows[blocks[bi]])>1 else ""
-    plain=fn.split("ILi")[0]
+    plain=os.environ.get("NCU_KERNEL", fn.split("ILi")[0])  # e.g. "dt_rmq_kernel<2,"
     if plain in name.replace(" ","") or plain in name:
         sel=(blocks[bi],blocks[bi+1]); break
 if sel is None: sel=(blocks[0],blocks[1])
