@@ -364,14 +364,37 @@ __device__ __forceinline__ constexpr bool exact_channel(int c) {
 
 // Trilinear weights in corner order k (bit0 x, bit1 y, bit2 z): w_k = (wx*wy)*wz
 // (hash_grid.hpp:50-54); the wx*wy products are shared, the values are identical.
+// NGPRT_PACKED_WEIGHTS: the 12 products as 6 FMUL2 (each half rounds like FMUL;
+// the products only feed multiplies, so nothing can contract them).
+#ifndef NGPRT_PACKED_WEIGHTS
+#define NGPRT_PACKED_WEIGHTS 1
+#endif
+__device__ __forceinline__ unsigned long long mul_f32x2(unsigned long long a, float b0, float b1) {
+    unsigned long long b, r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __device__ __forceinline__ void corner_weights(const float f[3], float w[8]) {
     const float wx[2] = {1.0f - f[0], f[0]}, wy[2] = {1.0f - f[1], f[1]},
                 wz[2] = {1.0f - f[2], f[2]};
+#if NGPRT_PACKED_WEIGHTS
+    unsigned long long x;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(wx[0]), "f"(wx[1]));
+    const unsigned long long a = mul_f32x2(x, wy[0], wy[0]);  // (wxy0, wxy1)
+    const unsigned long long b = mul_f32x2(x, wy[1], wy[1]);  // (wxy2, wxy3)
+    const unsigned long long p[4] = {mul_f32x2(a, wz[0], wz[0]), mul_f32x2(b, wz[0], wz[0]),
+                                     mul_f32x2(a, wz[1], wz[1]), mul_f32x2(b, wz[1], wz[1])};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(w[2 * q]), "=f"(w[2 * q + 1]) : "l"(p[q]));
+#else
     float wxy[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) wxy[j] = wx[j & 1] * wy[j >> 1];
 #pragma unroll
     for (int k = 0; k < 8; ++k) w[k] = wxy[k & 3] * wz[k >> 2];
+#endif
 }
 
 // Interpolate fine level l at x (hash_grid.hpp:97-106: out[c] = sum_k w_k row_k[c],
