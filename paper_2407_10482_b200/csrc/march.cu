@@ -356,6 +356,22 @@ __device__ __forceinline__ void mac2(bool fma, float& a0, float& a1, float w, fl
     }
 }
 
+// NGPRT_FHFMA (tensor-MLP mode, fp16 rows): a pair of colour channels takes
+// sm_100's mixed-precision FFMA (FHFMA: f32 += f16 x f16) straight on the raw
+// half2 row word with the trilinear weight rounded to f16: no f16 -> f32
+// conversions; the products are exact, so the only change is the weight's
+// rounding (relative 2^-11). Exact channels keep the f32 path.
+#ifndef NGPRT_FHFMA
+#define NGPRT_FHFMA 0
+#endif
+__device__ __forceinline__ uint16_t weight_f16(float w) { return __half_as_ushort(__float2half_rn(w)); }
+__device__ __forceinline__ void fhfma_pair(float& a0, float& a1, uint32_t raw, uint16_t w16) {
+    uint16_t lo, hi;
+    asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(raw));
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(a0) : "h"(lo), "h"(w16));
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(a1) : "h"(hi), "h"(w16));
+}
+
 // Coarse decoder channels that must stay exact: sigma_pre (0) and the omega
 // logits (8 + 2l), which set the density fuse weights of the variant modes.
 __device__ __forceinline__ constexpr bool exact_channel(int c) {
@@ -418,6 +434,25 @@ __device__ __forceinline__ void fine_level(const DevScene& sc, int l, const floa
         const uint32_t mask = sc.fine_mask[l];
         const uint32_t hy[2] = {uint32_t(b[1]) * 2654435761u, uint32_t(b[1] + 1) * 2654435761u};
         const uint32_t hz[2] = {uint32_t(b[2]) * 805459861u, uint32_t(b[2] + 1) * 805459861u};
+        if constexpr (F16 && FC && NGPRT_FHFMA) {
+            uint4 raw[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t row = (uint32_t(b[0] + (k & 1)) ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & mask;
+                NG_BOUNDS(row < sc.fine_len[l]);
+                raw[k] = ldg_fine(reinterpret_cast<const uint4*>(table) + row);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float2 v0 = __half22float2(*reinterpret_cast<const __half2*>(&raw[k].x));
+                mac2x(fine[0], fine[1], w[k], w[k], v0.x, v0.y);
+                const uint16_t w16 = weight_f16(w[k]);
+                fhfma_pair(fine[2], fine[3], raw[k].y, w16);
+                fhfma_pair(fine[4], fine[5], raw[k].z, w16);
+                fhfma_pair(fine[6], fine[7], raw[k].w, w16);
+            }
+            return;
+        }
         float frow[8][8];
 #if NGPRT_FINE_PAIR & 2
         if constexpr (F16) {
@@ -747,7 +782,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
                 const float2 v = F16 ? __half22float2(*reinterpret_cast<const __half2*>(&craw[k][i]))
                                      : make_float2(__uint_as_float(craw[k][2 * i]),
                                                    __uint_as_float(craw[k][2 * i + 1]));
-                if (FC && !exact_channel(2 * i) && !exact_channel(2 * i + 1))
+                if (FC && F16 && NGPRT_FHFMA && !exact_channel(2 * i) && !exact_channel(2 * i + 1))
+                    fhfma_pair(dec[2 * i], dec[2 * i + 1], craw[k][i], weight_f16(w[k]));
+                else if (FC && !exact_channel(2 * i) && !exact_channel(2 * i + 1))
                     mac2(true, dec[2 * i], dec[2 * i + 1], w[k], v.x, v.y);
                 else  // an exact channel's partner is exact too (one packed pair)
                     mac2x(dec[2 * i], dec[2 * i + 1], w[k], w[k], v.x, v.y);
@@ -804,7 +841,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
                 const float2 v = F16 ? __half22float2(*reinterpret_cast<const __half2*>(&fraw[l][k][i]))
                                      : make_float2(__uint_as_float(fraw[l][k][2 * i]),
                                                    __uint_as_float(fraw[l][k][2 * i + 1]));
-                if (FC && i != 0)
+                if (FC && F16 && NGPRT_FHFMA && i != 0)
+                    fhfma_pair(fine[2 * i], fine[2 * i + 1], fraw[l][k][i], weight_f16(w[k]));
+                else if (FC && i != 0)
                     mac2(true, fine[2 * i], fine[2 * i + 1], w[k], v.x, v.y);
                 else
                     mac2x(fine[2 * i], fine[2 * i + 1], w[k], w[k], v.x, v.y);
@@ -837,7 +876,9 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float2 v = __half22float2(h[i]);
-                if (FC && i != 0)
+                if (FC && NGPRT_FHFMA && i != 0)
+                    fhfma_pair(fine[2 * i], fine[2 * i + 1], (&r.x)[i], weight_f16(w[k]));
+                else if (FC && i != 0)
                     mac2(true, fine[2 * i], fine[2 * i + 1], w[k], v.x, v.y);
                 else
                     mac2x(fine[2 * i], fine[2 * i + 1], w[k], w[k], v.x, v.y);
