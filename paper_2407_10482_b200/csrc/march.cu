@@ -116,19 +116,41 @@ __device__ __forceinline__ int voxel_1d(float x, float h, int res) {
 }
 // Same for a point already clamped to [-1, 1]: u = (x + 1) * h >= +0, so only
 // the upper clamp (x == 1 -> u == res) can apply.
+// NGPRT_MAGIC_FLOOR: floor of a u in [0, 2^23) as the low mantissa bits of
+// RD(u + 2^23) (FADD.RM + IADD at full rate) instead of F2I / I2F conversions
+// (quarter-rate pipe); the float of a clamped index the same way. Exact.
+#ifndef NGPRT_MAGIC_FLOOR
+#define NGPRT_MAGIC_FLOOR 0
+#endif
+constexpr float kTwo23 = 8388608.0f;
+__device__ __forceinline__ int floor_nonneg(float u) {  // u in [0, 2^23)
+#if NGPRT_MAGIC_FLOOR
+    return __float_as_int(__fadd_rd(u, kTwo23)) - 0x4B000000;
+#else
+    return __float2int_rd(u);
+#endif
+}
+__device__ __forceinline__ float float_of_index(int i) {  // i in [0, 2^23)
+#if NGPRT_MAGIC_FLOOR
+    return __int_as_float(i + 0x4B000000) - kTwo23;
+#else
+    return float(i);
+#endif
+}
 __device__ __forceinline__ int voxel_1d_clamped(float x, float h, int res) {
-    const int i = __float2int_rd((x - (-1.0f)) * h);
+    const int i = floor_nonneg((x - (-1.0f)) * h);  // x in [-1, 1]: u in [0, res]
     return i > res - 1 ? res - 1 : i;
 }
 
 // Stencil along one axis: base index and fractional offset (hash_grid.hpp:38-46).
 __device__ __forceinline__ void stencil_axis(float x, float h, int res, int& base, float& frac) {
     const float u = (x - (-1.0f)) * h;
-    int i = __float2int_rd(u);
+    // (u clamped to [0, 2^22] for the floor only: outside [0, res) the index
+    // clamps to 0 or res - 1 either way; frac uses u itself)
+    int i = floor_nonneg(fminf(fmaxf(u, 0.0f), 4194304.0f));
     i = i < res - 1 ? i : res - 1;
-    i = i > 0 ? i : 0;
     base = i;
-    frac = u - float(i);
+    frac = u - float_of_index(i);
 }
 
 // L1 allocation policy of the fine-row and probe-code gathers (tuning;
