@@ -192,6 +192,20 @@ def test_distance_grid_u8_passes_match_reference(ng, torch, monkeypatch, depth):
             assert want[-1] == 254
 
 
+@pytest.mark.parametrize("res,dens,seed", [(288, 1e-5, 41), (300, 0.01, 42), (512, 2e-6, 43)])
+def test_distance_grid_above_256_matches_reference(ng, torch, res, dens, seed):
+    """r > 256 takes the u16 passes (pass X per row, envelope sweeps with u16
+    stack indices up to r = 1024): byte-identical to the reference."""
+    from checkers import ref
+    R = ref()
+    assert R is not None, "compiled reference (oracle/_ref) required"
+    words = random_grid_words(ng, res, dens, seed)
+    want = np.zeros(res ** 3, np.uint8)
+    R.ref_build_distance_grid(words.ctypes.data, res, want.ctypes.data)
+    got = ng.build_distance_grid(torch.from_numpy(words.view(np.int64)).cuda(), res).cpu().numpy()
+    assert np.array_equal(got, want), int((got != want).sum())
+
+
 def test_pyramid_matches_oracle_on_random_grids(ng, torch):
     from checkers import oracle
     O = oracle()
