@@ -53,12 +53,18 @@ __device__ __forceinline__ void mac_pair_exact(float& a0, float& a1, float w0, f
 // out[0..63] = b[0..63] + sum_c Wt[c][0..63] * in[c], c ascending. The inputs
 // come from this thread's shared-memory column (in[c * kShadeBlock]), so the c
 // loop stays rolled without spilling a register array to local memory.
+// NGPRT_EXACT_C_UNROLL: inputs per rolled-loop iteration (2: the next input's
+// weight loads are scheduled under the current input's multiply-adds).
+#ifndef NGPRT_EXACT_C_UNROLL
+#define NGPRT_EXACT_C_UNROLL 2
+#endif
+constexpr int kExactCUnroll = NGPRT_EXACT_C_UNROLL;
 template <int K>
 __device__ __forceinline__ void dense64(const float* __restrict__ wt, const float* __restrict__ b,
                                         const float* in, float* out) {
 #pragma unroll
     for (int o = 0; o < 64; ++o) out[o] = b[o];
-#pragma unroll 1
+#pragma unroll kExactCUnroll
     for (int c = 0; c < K; ++c) {
         const float x = in[c * kShadeBlock];
         const float4* row = reinterpret_cast<const float4*>(wt + c * 64);
