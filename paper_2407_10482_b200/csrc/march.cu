@@ -958,6 +958,11 @@ constexpr uint32_t kIdxMask = NGPRT_EXIT_FLAG ? 0x7fffffffu : 0xffffffffu;
 #ifndef NGPRT_STREAM_HINTS
 #define NGPRT_STREAM_HINTS 0
 #endif
+// NGPRT_TWO_RAYS (experiment, march_kernel): two rays per lane; 2 also switches
+// rays inside a step burst.
+#ifndef NGPRT_TWO_RAYS
+#define NGPRT_TWO_RAYS 0
+#endif
 // Per-lane ray state.
 // NGPRT_PROBE_REUSE: a lane keeps the last probe code and its level-1 voxel and
 // skips the load when the next marching point is in the same voxel (experiment).
@@ -1344,7 +1349,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks<L, F16>) march_kernel(const
     // 2L attention logits per thread (8L fine features in MLP fusion), then the
     // lane-state rows.
     constexpr int kAttRows = MLPF ? 8 * L : NGPRT_SCRATCH_ROWS;
-    __shared__ float scratch[kBlock * (kAttRows + kLaneRows)];
+    // NGPRT_TWO_RAYS: a second ray per lane (its lane rows, then its register
+    // fields: o, d, t, t1, T, out_idx, 4 counters)
+    constexpr int kAltRows = NGPRT_TWO_RAYS ? kLaneRows + 14 : 0;
+    __shared__ float scratch[kBlock * (kAttRows + kLaneRows + kAltRows)];
     constexpr int lb = kAttRows;  // first lane-state row
     constexpr int kStageLv = (F16 && !MLPF) ? kFineA<L> : 0;
     __shared__ uint4 fstage[kStageLv > 0 ? kStageLv * 8 * kBlock : 1];  // cp.async fine rows
@@ -1363,6 +1371,152 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks<L, F16>) march_kernel(const
     s.has_ray = false;
     s.pending = false;
 
+#if NGPRT_TWO_RAYS
+    // Two rays per lane (experiment): the ray in registers is the current one;
+    // the other's register fields sit in the lane's scratch rows at altb and
+    // its lane rows at lb + kLaneRows * (1 - cur). A lane whose current ray is
+    // parked steps its other ray, and a decode takes whichever ray is parked,
+    // so fewer lanes idle in either phase. Each ray still marches, decodes and
+    // composites in its own order, so results and counters are unchanged.
+    constexpr int altb = lb + 2 * kLaneRows;
+    int cur = 0;
+    bool alt_has = false, alt_pending = false;
+    auto swap_slot = [&]() {
+        auto sw = [&](float& f, int j) {
+            const float t = lane_row(scr, altb, j);
+            lane_row(scr, altb, j) = f;
+            f = t;
+        };
+        auto swu = [&](uint32_t& u, int j) {
+            float f = __uint_as_float(u);
+            sw(f, j);
+            u = __float_as_uint(f);
+        };
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            sw(s.ray.o[a], a);
+            sw(s.ray.d[a], 3 + a);
+        }
+        sw(s.t, 6);
+        sw(s.t1, 7);
+        sw(s.T, 8);
+        swu(s.out_idx, 9);
+        if constexpr (STATS) {
+            swu(s.n_march, 10);
+            swu(s.n_occ, 11);
+            swu(s.n_occ_acc, 12);
+            swu(s.n_dist, 13);
+        }
+        const bool h = s.has_ray, q = s.pending;
+        s.has_ray = alt_has;
+        s.pending = alt_pending;
+        alt_has = h;
+        alt_pending = q;
+        cur ^= 1;
+    };
+    auto refill = [&]() {  // the current slot of every lane without a ray
+        unsigned need = __ballot_sync(kFull, !s.has_ray);
+        while (need && !fetch_done) {
+            if (tile_next_slot == 32) {
+                uint32_t nt = 0;
+                if (lane == 0) nt = atomicAdd(p.work, 1u);
+                nt = __shfl_sync(kFull, nt, 0);
+                if (nt >= total_tiles) {
+                    fetch_done = true;
+                    break;
+                }
+                tile = nt;
+                tile_next_slot = 0;
+            }
+            const uint32_t avail = 32u - tile_next_slot;
+            const uint32_t take = min(uint32_t(__popc(need)), avail);
+            const uint32_t rank = __popc(need & lt_mask);
+            if (((need >> lane) & 1u) && rank < take)
+                start_ray(p, tile, tile_next_slot + rank, s, scr, lb + cur * kLaneRows);
+            tile_next_slot += take;
+            need = __ballot_sync(kFull, !s.has_ray);
+        }
+    };
+    while (true) {
+        if (!s.has_ray && alt_has) swap_slot();
+        refill();
+        if (!fetch_done) {
+            const bool want = s.has_ray && !alt_has;
+            if (__ballot_sync(kFull, want)) {
+                if (want) swap_slot();
+                refill();
+            }
+        }
+        const unsigned active = __ballot_sync(kFull, s.has_ray || alt_has);
+        if (!active) {
+            if (fetch_done) break;
+            continue;
+        }
+        const bool cur_parked = s.has_ray && s.pending, alt_parked = alt_has && alt_pending;
+        const bool cur_step = s.has_ray && !s.pending, alt_step = alt_has && !alt_pending;
+        const unsigned parked = __ballot_sync(kFull, cur_parked || alt_parked);
+        const unsigned stepping = __ballot_sync(kFull, cur_step || alt_step);
+        if (parked && (__popc(parked) >= p.decode_min || stepping == 0)) {
+            if (!cur_parked && alt_parked) swap_slot();
+            if (s.has_ray && s.pending) {
+                const int lbc = lb + cur * kLaneRows;
+                float f[8];
+                float xq[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) xq[a] = lane_row(scr, lbc, a);
+                if constexpr (!MLPF) {
+                    if (sc.fast_decode)
+                        decode_point_fast<L, FC, F16>(sc, xq, p.keep_level, tab, scr, stage, f);
+                    else
+                        decode_point<L, F16, MLPF>(sc, xq, p.keep_level, tab, scr, f);
+                } else {
+                    decode_point<L, F16, MLPF>(sc, xq, p.keep_level, tab, scr, f);
+                }
+                const float sigma = activate_density(f[0], tab);
+                const float a = alpha_from_sigma(sigma, step, tab);
+                const float w = a * s.T;
+                float c[7];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) c[j] = lane_row(scr, lbc, 3 + j);
+                c[0] = mac(FC, c[0], w, f[1]);
+                mac2(FC, c[1], c[2], w, f[2], f[3]);
+                mac2(FC, c[3], c[4], w, f[4], f[5]);
+                mac2(FC, c[5], c[6], w, f[6], f[7]);
+#pragma unroll
+                for (int j = 0; j < 7; ++j) lane_row(scr, lbc, 3 + j) = c[j];
+                s.T = s.T * (1.0f - a);
+                s.pending = false;
+                if (p.early_stop && s.T < float(2e-3)) {  // kEarlyStopTransmittance
+                    write_result(p, s, true, scr, lbc);
+                    s.has_ray = false;
+                } else {
+                    s.t += step;
+                }
+            }
+        } else {
+            if (!cur_step && alt_step) swap_slot();
+            if (s.has_ray && !s.pending) {
+#pragma unroll 1
+                for (int it = 0; it < p.step_burst; ++it) {
+                    const int lbc = lb + cur * kLaneRows;
+                    if (!march_point<STATS>(sc, p, s, scr, lbc)) {
+                        write_result(p, s, true, scr, lbc);
+                        s.has_ray = false;
+                        break;
+                    }
+                    if (s.pending) {
+                        if (NGPRT_TWO_RAYS >= 2 && alt_has && !alt_pending) {
+                            swap_slot();  // keep stepping with the other ray
+                            continue;
+                        }
+                        break;
+                    }
+                }
+            }
+        }
+    }
+    return;
+#endif
     while (true) {
         // ---- refill idle lanes from the warp's tile; fetch tiles as needed ----
         unsigned need = __ballot_sync(kFull, !s.has_ray);
