@@ -138,6 +138,9 @@ struct DevScene {
     uint32_t fine_mask[NGPRT_MAX_FINE_LEVELS];  // len-1 when len is a power of two <= 2^32
     int fine_mode[NGPRT_MAX_FINE_LEVELS];       // 0 direct, 1 hashed pow2, 2 hashed generic
     const void* coarse;   // dense (L_C+1)^3 rows x 16 elements (absent corners = zero rows)
+    // NGPRT_COARSE_CELLS (experiment): per coarse cell, its 8 corner rows' W fp16
+    // values back to back (16 W bytes per cell, L_C^3 cells), or null
+    const void* coarse_cells;
     const void* fine[NGPRT_MAX_FINE_LEVELS];    // table_len x 8 elements
     float att_w[2 * NGPRT_MAX_FINE_LEVELS];     // post-sigmoid global weights (Inv modes)
     int occ_res[NGPRT_PYRAMID_LEVELS];

@@ -709,7 +709,12 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
 #define NGPRT_COARSE_FULL_ROW 1
 #endif
     // u32 words of a coarse row actually loaded (W <= 12: 128+64-bit loads, else one 256-bit)
-    constexpr int CW = !F16 ? W : ((W <= 12 && !NGPRT_COARSE_FULL_ROW) ? 6 : 8);
+#if defined(NGPRT_COARSE_CELLS) && NGPRT_COARSE_CELLS
+    constexpr bool kCells = F16;  // fp16: the cell's 8 corner rows back to back (16 W bytes)
+#else
+    constexpr bool kCells = false;
+#endif
+    constexpr int CW = !F16 ? W : (kCells ? W / 2 : ((W <= 12 && !NGPRT_COARSE_FULL_ROW) ? 6 : 8));
     // ---- issue: coarse rows ----
     int cb[3];
     float cf[3];
@@ -718,6 +723,21 @@ __device__ __forceinline__ void decode_point_fast(const DevScene& sc, const floa
     const uint32_t r1 = uint32_t(sc.L_C) + 1;
     const uint32_t key0 = uint32_t(cb[0]) + r1 * (uint32_t(cb[1]) + r1 * uint32_t(cb[2]));
     uint32_t craw[8][CW];
+    if constexpr (kCells) {
+        const uint32_t lc = uint32_t(sc.L_C);
+        const uint32_t cell = uint32_t(cb[0]) + lc * (uint32_t(cb[1]) + lc * uint32_t(cb[2]));
+        const uint4* rec = reinterpret_cast<const uint4*>(sc.coarse_cells) + size_t(cell) * W;
+        uint32_t cw[W / 2][8];
+#pragma unroll
+        for (int q = 0; q < W / 2; ++q) ldg256(rec + 2 * q, cw[q]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int i = 0; i < W / 2; ++i) {
+                const int wi = k * (W / 2) + i;
+                craw[k][i] = cw[wi >> 3][wi & 7];
+            }
+    } else
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const uint32_t key = key0 + (k & 1) + ((k >> 1) & 1) * r1 + (k >> 2) * r1 * r1;

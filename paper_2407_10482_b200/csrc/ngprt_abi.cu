@@ -324,6 +324,17 @@ ngprt_status ngprt_scene_create(const ngprt_scene_desc* d, int device, ngprt_sce
             NG_TRY(cudaFreeAsync(drows, st));
         }
         ds.coarse = dense;
+#ifdef NGPRT_COARSE_CELLS
+        ds.coarse_cells = nullptr;
+        if (f16 && (w % 2) == 0) {
+            const size_t cb = size_t(d->L_C) * d->L_C * d->L_C * 16 * w;
+            void* cells;
+            NG_TRY(s->alloc(&cells, cb));
+            launch_coarse_cells(dense, int(d->L_C), int(w), cells, st);
+            NG_TRY(cudaGetLastError());
+            ds.coarse_cells = cells;
+        }
+#endif
     }
     // --- fine tables: one contiguous block (one L2 access-policy window) ---
     {

@@ -691,6 +691,22 @@ __global__ void scatter_coarse_kernel(const unsigned long long* __restrict__ key
     }
 }
 
+// Cell-brick copy of the fp16 coarse grid (NGPRT_COARSE_CELLS): thread = (cell,
+// corner k, word j) copies word j of corner k's row into the cell's record.
+__global__ void coarse_cells_kernel(const uint32_t* __restrict__ dense, int lc, int w2,
+                                    uint32_t* __restrict__ cells, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const size_t per_cell = size_t(8) * w2;
+        const size_t cell = i / per_cell;
+        const int r = int(i - cell * per_cell), k = r / w2, j = r - k * w2;
+        const size_t cx = cell % lc, cy = (cell / lc) % lc, cz = cell / (size_t(lc) * lc);
+        const size_t r1 = size_t(lc) + 1;
+        const size_t key = (cx + (k & 1)) + r1 * ((cy + ((k >> 1) & 1)) + r1 * (cz + (k >> 2)));
+        cells[i] = dense[key * 8 + j];  // a row is 16 fp16 = 8 words
+    }
+}
+
 __global__ void convert_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst,
                                    size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
@@ -796,6 +812,12 @@ void launch_scatter_coarse(const unsigned long long* keys, const float* rows, si
         scatter_coarse_kernel<true><<<blocks_for(n, 256), 256, 0, st>>>(keys, rows, n, w, dense);
     else
         scatter_coarse_kernel<false><<<blocks_for(n, 256), 256, 0, st>>>(keys, rows, n, w, dense);
+}
+
+void launch_coarse_cells(const void* dense_f16, int L_C, int w, void* cells, cudaStream_t st) {
+    const size_t n = size_t(L_C) * L_C * L_C * 8 * (w / 2);
+    coarse_cells_kernel<<<148 * 16, 256, 0, st>>>(static_cast<const uint32_t*>(dense_f16), L_C, w / 2,
+                                                  static_cast<uint32_t*>(cells), n);
 }
 
 void launch_convert_fine(const float* src, void* dst, size_t n, int f16, cudaStream_t st) {

@@ -125,6 +125,7 @@ void launch_distance_grid(const uint32_t* occ, int res, uint16_t* tmp_a, uint16_
 void launch_scatter_coarse(const unsigned long long* keys, const float* rows, size_t n, int w,
                            void* dense, int f16, cudaStream_t st);
 void launch_convert_fine(const float* src, void* dst, size_t n, int f16, cudaStream_t st);
+void launch_coarse_cells(const void* dense_f16, int L_C, int w, void* cells, cudaStream_t st);
 
 // test hooks
 void launch_test_expf(const float* x, float* y, size_t n, cudaStream_t st);
