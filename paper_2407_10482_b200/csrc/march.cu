@@ -978,6 +978,10 @@ constexpr uint32_t kIdxMask = NGPRT_EXIT_FLAG ? 0x7fffffffu : 0xffffffffu;
 #ifndef NGPRT_STREAM_HINTS
 #define NGPRT_STREAM_HINTS 0
 #endif
+// NGPRT_TILE_STRIP (experiment): ray-tile order, see start_ray (0: row-major)
+#ifndef NGPRT_TILE_STRIP
+#define NGPRT_TILE_STRIP 0
+#endif
 // NGPRT_TWO_RAYS (experiment, march_kernel): two rays per lane; 2 also switches
 // rays inside a step burst.
 #ifndef NGPRT_TWO_RAYS
@@ -1069,8 +1073,19 @@ __device__ __forceinline__ void start_ray(const MarchParams& p, uint32_t tile, u
         if (px >= p.w || py >= p.h) return;
         s.out_idx = ((cam * p.shard_local + j) * p.shard_tile + ly) * p.shard_tile + lx;
     } else {
+#if NGPRT_TILE_STRIP
+        // experiment: tiles column-major inside strips of NGPRT_TILE_STRIP tile rows,
+        // so the tiles in flight cover a compact 2D region instead of a row band
+        const uint32_t tiles_y = p.tiles_per_cam / p.tiles_x;
+        const uint32_t strip = tt / (NGPRT_TILE_STRIP * p.tiles_x);
+        const uint32_t r = tt - strip * NGPRT_TILE_STRIP * p.tiles_x;
+        const uint32_t hs = min(uint32_t(NGPRT_TILE_STRIP), tiles_y - strip * NGPRT_TILE_STRIP);
+        const uint32_t tx = r / hs, ty = strip * NGPRT_TILE_STRIP + r % hs;
+        const uint32_t px = tx * kRayTileW + (slot % kRayTileW), py = ty * kRayTileH + (slot / kRayTileW);
+#else
         const uint32_t px = (tt % p.tiles_x) * kRayTileW + (slot % kRayTileW),
                        py = (tt / p.tiles_x) * kRayTileH + (slot / kRayTileW);
+#endif
         if (px >= p.w || py >= p.h) return;
         s.out_idx = (cam * p.h + py) * p.w + px;
     }
