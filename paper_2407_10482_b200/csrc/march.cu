@@ -145,12 +145,20 @@ __device__ __forceinline__ int voxel_1d_clamped(float x, float h, int res) {
 // Stencil along one axis: base index and fractional offset (hash_grid.hpp:38-46).
 __device__ __forceinline__ void stencil_axis(float x, float h, int res, int& base, float& frac) {
     const float u = (x - (-1.0f)) * h;
+#if NGPRT_MAGIC_FLOOR
     // (u clamped to [0, 2^22] for the floor only: outside [0, res) the index
     // clamps to 0 or res - 1 either way; frac uses u itself)
     int i = floor_nonneg(fminf(fmaxf(u, 0.0f), 4194304.0f));
     i = i < res - 1 ? i : res - 1;
     base = i;
     frac = u - float_of_index(i);
+#else
+    int i = __float2int_rd(u);
+    i = i < res - 1 ? i : res - 1;
+    i = i > 0 ? i : 0;
+    base = i;
+    frac = u - float(i);
+#endif
 }
 
 // L1 allocation policy of the fine-row and probe-code gathers (tuning;
